@@ -1,0 +1,89 @@
+"""Stress-velocity Newton loop for one implicit time step (ORACLE).
+
+Test infrastructure only.  Follows PAPER.md in order:
+  * v_0 = v^n, pi_0 = tau(v^n)/Delta(v^n)                        (reading G4)
+  * solve J(v_l, pi_l) v~ = R(v_l)                               (eq:linearSVNewton)
+  * alpha = 1, 1/2, ... while Phi does not decrease                (G12, G14)
+  * v_{l+1} = v_l + alpha v~, pi_{l+1} = pi_l + alpha pi~          (eq:tautilde)
+  * stop at ||R(v_l)||_2 <= rtol ||R(v_0)||_2 (BASELINE.json 1e-8; the paper uses a
+    1e4 reduction), absolute floor 1e-14, maxit 200.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import krylov
+from .model import Problem
+
+
+def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
+               ls_max=20, krylov_rtol=1e-8, krylov_maxit=300, restart=30,
+               project_pi=False, amg_params=None, record_iterates=False):
+    pb = Problem(inp, prm)
+    v = pb.v_prev.copy()
+    v[pb.bdof] = 0.0
+    pi = pb.pi_consistent(v)
+    hist = {"res": [], "alpha": [], "dphi": [], "krylov": [], "halvings": [],
+            "stagnated": [], "iterates": []}
+    r0 = None
+    converged = False
+    for l in range(maxit + 1):
+        R = pb.residual(v)
+        nr = float(np.linalg.norm(R))
+        hist["res"].append(nr)
+        if record_iterates:
+            hist["iterates"].append((v.copy(), pi.copy()))
+        if r0 is None:
+            r0 = nr
+            if r0 < 1e-14:
+                converged = True
+                break
+        if nr <= rtol * r0:
+            converged = True
+            break
+        if l == maxit:
+            break
+        pi_j = pi if kind == "sv" else None
+        J = pb.jacobian(v, pi_j, kind)
+        if linsolve == "direct":
+            vt = krylov.sparse_direct_solve(J, R)
+            kst = {"iters": 0}
+        elif linsolve == "dense":
+            vt = krylov.dense_cholesky_solve(J, R)
+            kst = {"iters": 0}
+        elif linsolve == "jacobi_fgmres":
+            vt, kst = krylov.fgmres(lambda x: J @ x, R, krylov.jacobi(J), restart, krylov_rtol, krylov_maxit)
+        elif linsolve == "amg_fgmres":
+            from . import amg
+            H = amg.setup(J, pb, **(amg_params or {}))
+            vt, kst = krylov.fgmres(lambda x: J @ x, R, lambda r: amg.vcycle(H, r), restart,
+                                    krylov_rtol, krylov_maxit)
+            kst["levels"] = len(H["levels"])
+        else:
+            raise ValueError(linsolve)
+        hist["krylov"].append(kst)
+        alpha, dphi, stag, halv = 1.0, 0.0, True, 0
+        for k in range(ls_max + 1):
+            alpha = 0.5 ** k
+            dphi = pb.delta_energy(v, vt, alpha)
+            if dphi < 0.0:
+                stag = False
+                halv = k
+                break
+        else:
+            halv = ls_max
+        hist["alpha"].append(alpha)
+        hist["dphi"].append(dphi)
+        hist["halvings"].append(halv)
+        hist["stagnated"].append(stag)
+        if kind == "sv":
+            pt = pb.pi_tilde(v, pi, vt)
+            pi = pi + alpha * pt
+            if project_pi:
+                T = pb.pi_to_tensor(pi)
+                s = np.maximum(1.0, np.sqrt(2.0 * np.sum(T * T, axis=(-2, -1))))
+                pi = pb.pi_from_tensor(T / s[..., None, None])
+        v = v + alpha * vt
+    hist["newton_iters"] = len(hist["alpha"])
+    hist["converged"] = converged
+    return v, pi, hist

@@ -1,0 +1,628 @@
+// assembly.cu — per-step setup (K2, K22), fused residual + Jacobian assembly (K1),
+// line-search energy differences (K11) and the dual update (K12).
+//
+// All kernels are atomics-free gathers: one thread per node recomputes the
+// quadrature-point quantities of its (up to) four cells, so every matrix value
+// and residual entry is written exactly once by one thread (bitwise deterministic).
+#include <cmath>
+#include <vector>
+
+#include "ctx.cuh"
+
+namespace seaice {
+
+// ------------------------------------------------------------------ K2 / K22
+// P = P* h exp(-C (1-A)) (eq:ice-strength); rho_i h; range checks.
+__global__ void k_cell_setup(int Nc, Phys ph, const double* __restrict__ h, const double* __restrict__ A,
+                             double* __restrict__ P, double* __restrict__ rhoh, int* __restrict__ flag) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= Nc) return;
+  double hc = h[c], Ac = A[c];
+  bool bad = !(isfinite(hc) && isfinite(Ac) && hc >= 0.0 && Ac >= 0.0 && Ac <= 1.0);
+  if (bad) atomicOr(flag, 1);
+  P[c] = ph.P_star * hc * exp(-ph.C * (1.0 - Ac));
+  rhoh[c] = ph.rho_i * hc;
+}
+
+__global__ void k_check_finite(long long n, const double* __restrict__ x, int* __restrict__ flag, int bit) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n && !isfinite(x[i])) atomicOr(flag, bit);
+}
+
+// Load the 4 nodal 2-vectors of cell (ci,cj).
+__device__ __forceinline__ void load_cell_vec(const double* __restrict__ x, int n, int ci, int cj, double u[4][2]) {
+  const int s = n + 1;
+  const int n0 = cj * s + ci;
+  const int ids[4] = {n0, n0 + 1, n0 + s + 1, n0 + s};
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    double2 t = __ldg(reinterpret_cast<const double2*>(x) + ids[b]);
+    u[b][0] = t.x;
+    u[b][1] = t.y;
+  }
+}
+
+// F(phi_{a,k}) contributions of one cell to local node AL (eq:F):
+//   sum_q w N_a [rho h v^n - dt rho h f_c e_r x (v^n - v_o) + dt tau_atm(v_a)]_k
+template <int AL>
+__device__ __forceinline__ void force_cell(const Phys& ph, int ci, int cj, const double* __restrict__ vn,
+                                           const double* __restrict__ vo, const double* __restrict__ va,
+                                           const double* __restrict__ rhoh, double& f0, double& f1) {
+  double un[4][2], uo[4][2], ua[4][2];
+  load_cell_vec(vn, ph.n, ci, cj, un);
+  load_cell_vec(vo, ph.n, ci, cj, uo);
+  load_cell_vec(va, ph.n, ci, cj, ua);
+  const double rh = rhoh[cj * ph.n + ci];
+  const double w = 0.25 * ph.dx * ph.dx;
+  const double ca = ph.C_a * ph.rho_a;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double vnx = 0, vny = 0, vox = 0, voy = 0, vax = 0, vay = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const double N = Nq(q, b);
+      vnx += N * un[b][0]; vny += N * un[b][1];
+      vox += N * uo[b][0]; voy += N * uo[b][1];
+      vax += N * ua[b][0]; vay += N * ua[b][1];
+    }
+    const double sa = ca * sqrt(vax * vax + vay * vay);
+    const double dux = vnx - vox, duy = vny - voy;
+    // e_r x u = (-u_y, u_x)
+    const double gxv = rh * vnx - ph.dt * rh * ph.f_c * (-duy) + ph.dt * sa * vax;
+    const double gyv = rh * vny - ph.dt * rh * ph.f_c * (dux) + ph.dt * sa * vay;
+    const double wn = w * Nq(q, AL);
+    f0 += wn * gxv;
+    f1 += wn * gyv;
+  }
+}
+
+__global__ void k_force(Phys ph, int Nn, const double* __restrict__ vn, const double* __restrict__ vo,
+                        const double* __restrict__ va, const double* __restrict__ rhoh,
+                        const double* __restrict__ load, double* __restrict__ F) {
+  int node = blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= Nn) return;
+  const int s = ph.n + 1;
+  const int i = node % s, j = node / s;
+  double f0 = 0.0, f1 = 0.0;
+  if (i > 0 && i < ph.n && j > 0 && j < ph.n) {
+    force_cell<2>(ph, i - 1, j - 1, vn, vo, va, rhoh, f0, f1);
+    force_cell<3>(ph, i, j - 1, vn, vo, va, rhoh, f0, f1);
+    force_cell<1>(ph, i - 1, j, vn, vo, va, rhoh, f0, f1);
+    force_cell<0>(ph, i, j, vn, vo, va, rhoh, f0, f1);
+    if (load) {
+      f0 += load[2 * node];
+      f1 += load[2 * node + 1];
+    }
+  }
+  F[2 * node] = f0;
+  F[2 * node + 1] = f1;
+}
+
+// Velocity gradient of a Q1 field at Gauss point q (physical, 1/dx applied).
+template <int Q>
+__device__ __forceinline__ void grad_at(const double u[4][2], double inv_dx, double& L00, double& L01, double& L10,
+                                        double& L11) {
+  L00 = L01 = L10 = L11 = 0.0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    L00 += u[b][0] * Gx(Q, b);
+    L01 += u[b][0] * Gy(Q, b);
+    L10 += u[b][1] * Gx(Q, b);
+    L11 += u[b][1] * Gy(Q, b);
+  }
+  L00 *= inv_dx; L01 *= inv_dx; L10 *= inv_dx; L11 *= inv_dx;
+}
+
+// pi = tau(v^n)/Delta(v^n) at every Gauss point (eq:pi; reading G4).
+__global__ void k_pi_init(Phys ph, int Nc, const double* __restrict__ v, double* __restrict__ pi) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= Nc) return;
+  const int ci = c % ph.n, cj = c / ph.n;
+  double u[4][2];
+  load_cell_vec(v, ph.n, ci, cj, u);
+  const double inv_dx = 1.0 / ph.dx, inv_e = 1.0 / ph.e;
+  double L00, L01, L10, L11;
+#define PI_Q(Q)                                                                  \
+  {                                                                              \
+    grad_at<Q>(u, inv_dx, L00, L01, L10, L11);                                   \
+    V3 t = tau_hat_grad(L00, L01, L10, L11, inv_e);                              \
+    const double D = sqrt(ph.delta_min * ph.delta_min + 2.0 * dot3(t, t));      \
+    V3 p{t.x / D, t.y / D, t.z / D};                                             \
+    double p11, p12, p22;                                                        \
+    from_hat(p, p11, p12, p22);                                                  \
+    pi[(0 * 4 + Q) * (long long)Nc + c] = p11;                                   \
+    pi[(1 * 4 + Q) * (long long)Nc + c] = p12;                                   \
+    pi[(2 * 4 + Q) * (long long)Nc + c] = p22;                                   \
+  }
+  PI_Q(0) PI_Q(1) PI_Q(2) PI_Q(3)
+#undef PI_Q
+}
+
+// ------------------------------------------------------------------ K1
+// Contribution of one cell to the two residual rows and 2x8 Jacobian row block of
+// its local node AL (eq:A + eq:sigma for R; eq:linearSVNewton/-modification for K):
+//   R_k  -= sum_q w [rho h v_k N_a + dt (P/Delta) tau^(v).tau^(N_a e_k) - dt (P/2) dN_a/dx_k
+//                    - dt C_o rho_o |w| w_k N_a]
+//   K_km += sum_q w [rho h N_a N_b d_km + dt tau^(N_a e_k).C tau^(N_b e_m) + dt N_a N_b D_km]
+template <int KIND, bool JAC, int AL>
+__device__ __forceinline__ void assemble_cell(const Phys& ph, int ci, int cj, const double* __restrict__ v,
+                                              const double* __restrict__ pi, const double* __restrict__ P,
+                                              const double* __restrict__ rhoh, const double* __restrict__ vo,
+                                              double acc[36], double& r0, double& r1) {
+  const int n = ph.n;
+  const long long Nc = (long long)n * n;
+  const int cell = cj * n + ci;
+  double u[4][2], uo[4][2];
+  load_cell_vec(v, n, ci, cj, u);
+  load_cell_vec(vo, n, ci, cj, uo);
+  const double Pc = P[cell], rh = rhoh[cell];
+  const double inv_dx = 1.0 / ph.dx, inv_e = 1.0 / ph.e;
+  const double w = 0.25 * ph.dx * ph.dx;
+  const double co = ph.C_o * ph.rho_o;
+  const double dt = ph.dt;
+  const double dmin2 = ph.delta_min * ph.delta_min;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double vx = 0, vy = 0, ox_ = 0, oy_ = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      vx += Nq(q, b) * u[b][0];
+      vy += Nq(q, b) * u[b][1];
+      ox_ += Nq(q, b) * uo[b][0];
+      oy_ += Nq(q, b) * uo[b][1];
+    }
+    double L00 = 0, L01 = 0, L10 = 0, L11 = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      L00 += u[b][0] * Gx(q, b);
+      L01 += u[b][0] * Gy(q, b);
+      L10 += u[b][1] * Gx(q, b);
+      L11 += u[b][1] * Gy(q, b);
+    }
+    L00 *= inv_dx; L01 *= inv_dx; L10 *= inv_dx; L11 *= inv_dx;
+    const V3 t = tau_hat_grad(L00, L01, L10, L11, inv_e);
+    const double D = sqrt(dmin2 + 2.0 * dot3(t, t));
+    const double c0 = Pc / D;
+    // ocean drag
+    const double wx = ox_ - vx, wy = oy_ - vy;
+    const double nw = sqrt(wx * wx + wy * wy);
+    // test-function tau^ of node AL
+    const double gxa = Gx(q, AL) * inv_dx, gya = Gy(q, AL) * inv_dx;
+    const V3 ta0 = tau_hat_ex(gxa, gya, inv_e);
+    const V3 ta1 = tau_hat_ey(gxa, gya, inv_e);
+    const double Na = Nq(q, AL);
+    // residual: R -= A(v, phi)
+    r0 -= w * (rh * vx * Na + dt * c0 * dot3(t, ta0) - dt * 0.5 * Pc * gxa - dt * co * nw * wx * Na);
+    r1 -= w * (rh * vy * Na + dt * c0 * dot3(t, ta1) - dt * 0.5 * Pc * gya - dt * co * nw * wy * Na);
+    if (JAC) {
+      // u_k = C tau^(N_a e_k)
+      V3 u0 = ta0, u1 = ta1;
+      u0.x *= c0; u0.y *= c0; u0.z *= c0;
+      u1.x *= c0; u1.y *= c0; u1.z *= c0;
+      if (KIND == SEAICE_JAC_SV) {
+        const V3 p = pi_hat(pi[(0 * 4 + q) * Nc + cell], pi[(1 * 4 + q) * Nc + cell], pi[(2 * 4 + q) * Nc + cell]);
+        const double s = fmax(1.0, kR2 * sqrt(dot3(p, p)));
+        const double c1 = Pc / (D * D * s);
+        const double tt0 = dot3(t, ta0), pt0 = dot3(p, ta0);
+        const double tt1 = dot3(t, ta1), pt1 = dot3(p, ta1);
+        u0.x -= c1 * (p.x * tt0 + t.x * pt0); u0.y -= c1 * (p.y * tt0 + t.y * pt0); u0.z -= c1 * (p.z * tt0 + t.z * pt0);
+        u1.x -= c1 * (p.x * tt1 + t.x * pt1); u1.y -= c1 * (p.y * tt1 + t.y * pt1); u1.z -= c1 * (p.z * tt1 + t.z * pt1);
+      } else if (KIND == SEAICE_JAC_STD) {
+        const double c1 = 2.0 * Pc / (D * D * D);
+        const double tt0 = dot3(t, ta0), tt1 = dot3(t, ta1);
+        u0.x -= c1 * t.x * tt0; u0.y -= c1 * t.y * tt0; u0.z -= c1 * t.z * tt0;
+        u1.x -= c1 * t.x * tt1; u1.y -= c1 * t.y * tt1; u1.z -= c1 * t.z * tt1;
+      }
+      // drag coefficient D_km = C_o rho_o (|w| d_km + w_k w_m / |w|), rank-one part dropped if |w| < 1e-12
+      double d00 = co * nw, d11 = co * nw, d01 = 0.0;
+      if (nw >= 1e-12) {
+        const double inw = co / nw;
+        d00 += inw * wx * wx;
+        d11 += inw * wy * wy;
+        d01 = inw * wx * wy;
+      }
+      const double wdt = w * dt;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int sl = slot_ab(AL, b);
+        const double gxb = Gx(q, b) * inv_dx, gyb = Gy(q, b) * inv_dx;
+        const V3 tb0 = tau_hat_ex(gxb, gyb, inv_e);
+        const V3 tb1 = tau_hat_ey(gxb, gyb, inv_e);
+        const double NN = Na * Nq(q, b);
+        const double mass = w * rh * NN;
+        acc[sl * 4 + 0] += mass + wdt * (dot3(u0, tb0) + NN * d00);
+        acc[sl * 4 + 1] += wdt * (dot3(u0, tb1) + NN * d01);
+        acc[sl * 4 + 2] += wdt * (dot3(u1, tb0) + NN * d01);
+        acc[sl * 4 + 3] += mass + wdt * (dot3(u1, tb1) + NN * d11);
+      }
+    }
+  }
+}
+
+template <int KIND, bool JAC>
+__global__ void __launch_bounds__(128) k_assemble(Phys ph, int Nn, const double* __restrict__ v,
+                                                  const double* __restrict__ pi, const double* __restrict__ P,
+                                                  const double* __restrict__ rhoh, const double* __restrict__ vo,
+                                                  const double* __restrict__ F, double* __restrict__ Jst,
+                                                  double* __restrict__ R, double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int node = blockIdx.x * blockDim.x + threadIdx.x;
+  double nrm = 0.0;
+  if (node < Nn) {
+    const int s = ph.n + 1;
+    const int i = node % s, j = node / s;
+    const bool interior = (i > 0 && i < ph.n && j > 0 && j < ph.n);
+    if (!interior) {
+      if (JAC) {
+#pragma unroll
+        for (int e = 0; e < 36; ++e) Jst[(long long)e * Nn + node] = (e == 16 || e == 19) ? 1.0 : 0.0;
+      }
+      R[2 * node] = 0.0;
+      R[2 * node + 1] = 0.0;
+    } else {
+      double acc[36];
+#pragma unroll
+      for (int e = 0; e < 36; ++e) acc[e] = 0.0;
+      double r0 = F[2 * node], r1 = F[2 * node + 1];
+      assemble_cell<KIND, JAC, 2>(ph, i - 1, j - 1, v, pi, P, rhoh, vo, acc, r0, r1);
+      assemble_cell<KIND, JAC, 3>(ph, i, j - 1, v, pi, P, rhoh, vo, acc, r0, r1);
+      assemble_cell<KIND, JAC, 1>(ph, i - 1, j, v, pi, P, rhoh, vo, acc, r0, r1);
+      assemble_cell<KIND, JAC, 0>(ph, i, j, v, pi, P, rhoh, vo, acc, r0, r1);
+      R[2 * node] = r0;
+      R[2 * node + 1] = r1;
+      nrm = r0 * r0 + r1 * r1;
+      if (JAC) {
+#pragma unroll
+        for (int sl = 0; sl < 9; ++sl) {
+          const int ii = i + (sl % 3) - 1, jj = j + (sl / 3) - 1;
+          const bool bnd = (ii == 0 || ii == ph.n || jj == 0 || jj == ph.n);  // symmetric elimination
+#pragma unroll
+          for (int e = 0; e < 4; ++e) Jst[(long long)(sl * 4 + e) * Nn + node] = bnd ? 0.0 : acc[sl * 4 + e];
+        }
+      }
+    }
+  }
+  double bs = block_sum(nrm, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = bs;
+}
+
+// ------------------------------------------------------------------ K11
+// Phi(v + a vt) - Phi(v) per alpha, difference form (reading G12; eq:energy P:261-268).
+constexpr int kMaxAlpha = 8;
+__global__ void __launch_bounds__(128) k_delta_energy(Phys ph, int Nc, const double* __restrict__ v,
+                                                      const double* __restrict__ vt, const double* __restrict__ vn,
+                                                      const double* __restrict__ vo, const double* __restrict__ va,
+                                                      const double* __restrict__ P, const double* __restrict__ rhoh,
+                                                      const double* __restrict__ alphas_d, int count,
+                                                      double* __restrict__ part) {
+  __shared__ double sh[32];
+  double acc[kMaxAlpha];
+  double al[kMaxAlpha];
+#pragma unroll
+  for (int k = 0; k < kMaxAlpha; ++k) {
+    acc[k] = 0.0;
+    al[k] = (k < count) ? alphas_d[k] : 0.0;
+  }
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < Nc) {
+    const int n = ph.n, ci = c % n, cj = c / n;
+    double u[4][2], ut[4][2], un[4][2], uo[4][2], ua[4][2];
+    load_cell_vec(v, n, ci, cj, u);
+    load_cell_vec(vt, n, ci, cj, ut);
+    load_cell_vec(vn, n, ci, cj, un);
+    load_cell_vec(vo, n, ci, cj, uo);
+    load_cell_vec(va, n, ci, cj, ua);
+    const double Pc = P[c], rh = rhoh[c];
+    const double inv_dx = 1.0 / ph.dx, inv_e = 1.0 / ph.e;
+    const double w = 0.25 * ph.dx * ph.dx, dt = ph.dt;
+    const double co3 = ph.C_o * ph.rho_o / 3.0, ca = ph.C_a * ph.rho_a;
+    const double dmin2 = ph.delta_min * ph.delta_min;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double x0 = 0, y0 = 0, xt = 0, yt = 0, xn = 0, yn = 0, xo = 0, yo = 0, xa = 0, ya = 0;
+      double A00 = 0, A01 = 0, A10 = 0, A11 = 0, B00 = 0, B01 = 0, B10 = 0, B11 = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const double N = Nq(q, b);
+        x0 += N * u[b][0]; y0 += N * u[b][1];
+        xt += N * ut[b][0]; yt += N * ut[b][1];
+        xn += N * un[b][0]; yn += N * un[b][1];
+        xo += N * uo[b][0]; yo += N * uo[b][1];
+        xa += N * ua[b][0]; ya += N * ua[b][1];
+        A00 += u[b][0] * Gx(q, b); A01 += u[b][0] * Gy(q, b); A10 += u[b][1] * Gx(q, b); A11 += u[b][1] * Gy(q, b);
+        B00 += ut[b][0] * Gx(q, b); B01 += ut[b][0] * Gy(q, b); B10 += ut[b][1] * Gx(q, b); B11 += ut[b][1] * Gy(q, b);
+      }
+      const V3 t0 = tau_hat_grad(A00 * inv_dx, A01 * inv_dx, A10 * inv_dx, A11 * inv_dx, inv_e);
+      const V3 tt = tau_hat_grad(B00 * inv_dx, B01 * inv_dx, B10 * inv_dx, B11 * inv_dx, inv_e);
+      const double trt = (B00 + B11) * inv_dx;
+      const double D0 = sqrt(dmin2 + 2.0 * dot3(t0, t0));
+      const double w0x = xo - x0, w0y = yo - y0;
+      const double n0 = sqrt(w0x * w0x + w0y * w0y);
+      const double sa = ca * sqrt(xa * xa + ya * ya);
+      // linear terms: rho h f_c (e_r x (v^n - v_o)).vt - tau_atm.vt
+      const double dux = xn - xo, duy = yn - yo;
+      const double lin = rh * ph.f_c * (-duy * xt + dux * yt) - sa * (xa * xt + ya * yt);
+      const double vtv0 = xt * x0 + yt * y0, vtvt = xt * xt + yt * yt, vnvt = xn * xt + yn * yt;
+      const double tt_t0 = dot3(tt, t0), tt_tt = dot3(tt, tt);
+#pragma unroll
+      for (int k = 0; k < kMaxAlpha; ++k) {
+        if (k < count) {
+          const double a = al[k];
+          const double tmass = 0.5 * rh * a * (2.0 * vtv0 + a * vtvt) - rh * a * vnvt;
+          const V3 t1{t0.x + a * tt.x, t0.y + a * tt.y, t0.z + a * tt.z};
+          const double D1 = sqrt(dmin2 + 2.0 * dot3(t1, t1));
+          const double dD = 2.0 * a * (2.0 * tt_t0 + a * tt_tt) / (D1 + D0);
+          const double tpl = 0.5 * Pc * (dD - a * trt);
+          const double w1x = w0x - a * xt, w1y = w0y - a * yt;
+          const double n1 = sqrt(w1x * w1x + w1y * w1y);
+          const double den = n1 + n0;
+          const double dn = den > 0.0 ? ((w1x - w0x) * (w1x + w0x) + (w1y - w0y) * (w1y + w0y)) / den : 0.0;
+          const double toc = co3 * dn * (n1 * n1 + n1 * n0 + n0 * n0);
+          acc[k] += w * (tmass + dt * (tpl + toc + a * lin));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kMaxAlpha; ++k) {
+    if (k < count) {
+      double bs = block_sum(acc[k], sh);
+      if (threadIdx.x == 0) part[(long long)k * gridDim.x + blockIdx.x] = bs;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K12
+// pi~ = -pi + tau/Delta + tau(vt)/Delta - [(tau.tau(vt)) pi + (pi.tau(vt)) tau]/(s Delta^2)
+// (eq:tautilde P:504-511 with eq:modification).  mode 0: out = pi~;
+// mode 1: out = pi + alpha pi~ (in place allowed), optionally projected (reading G5 flag).
+__global__ void k_pi_tilde(Phys ph, int Nc, const double* __restrict__ v, const double* pi,
+                           const double* __restrict__ vt, double* out, double alpha, int mode, int project) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= Nc) return;
+  const int n = ph.n, ci = c % n, cj = c / n;
+  double u[4][2], ut[4][2];
+  load_cell_vec(v, n, ci, cj, u);
+  load_cell_vec(vt, n, ci, cj, ut);
+  const double inv_dx = 1.0 / ph.dx, inv_e = 1.0 / ph.e;
+  const double dmin2 = ph.delta_min * ph.delta_min;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double A00 = 0, A01 = 0, A10 = 0, A11 = 0, B00 = 0, B01 = 0, B10 = 0, B11 = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      A00 += u[b][0] * Gx(q, b); A01 += u[b][0] * Gy(q, b); A10 += u[b][1] * Gx(q, b); A11 += u[b][1] * Gy(q, b);
+      B00 += ut[b][0] * Gx(q, b); B01 += ut[b][0] * Gy(q, b); B10 += ut[b][1] * Gx(q, b); B11 += ut[b][1] * Gy(q, b);
+    }
+    const V3 t = tau_hat_grad(A00 * inv_dx, A01 * inv_dx, A10 * inv_dx, A11 * inv_dx, inv_e);
+    const V3 tt = tau_hat_grad(B00 * inv_dx, B01 * inv_dx, B10 * inv_dx, B11 * inv_dx, inv_e);
+    const double D = sqrt(dmin2 + 2.0 * dot3(t, t));
+    const long long i0 = (0 * 4 + q) * (long long)Nc + c, i1 = (1 * 4 + q) * (long long)Nc + c,
+                    i2 = (2 * 4 + q) * (long long)Nc + c;
+    const V3 p = pi_hat(pi[i0], pi[i1], pi[i2]);
+    const double s = fmax(1.0, kR2 * sqrt(dot3(p, p)));
+    const double iD = 1.0 / D;
+    const double k1 = dot3(t, tt) / (s * D * D), k2 = dot3(p, tt) / (s * D * D);
+    V3 pt{-p.x + (t.x + tt.x) * iD - (k1 * p.x + k2 * t.x), -p.y + (t.y + tt.y) * iD - (k1 * p.y + k2 * t.y),
+          -p.z + (t.z + tt.z) * iD - (k1 * p.z + k2 * t.z)};
+    V3 r = pt;
+    if (mode == 1) {
+      r = V3{p.x + alpha * pt.x, p.y + alpha * pt.y, p.z + alpha * pt.z};
+      if (project) {
+        const double sc = fmax(1.0, kR2 * sqrt(dot3(r, r)));
+        r.x /= sc; r.y /= sc; r.z /= sc;
+      }
+    }
+    double p11, p12, p22;
+    from_hat(r, p11, p12, p22);
+    out[i0] = p11;
+    out[i1] = p12;
+    out[i2] = p22;
+  }
+}
+
+// ------------------------------------------------------------------ CSR view
+__global__ void k_csr_values(int n, int Nn, const double* __restrict__ Jst, const int* __restrict__ rp,
+                             double* __restrict__ val) {
+  const int node = blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= Nn) return;
+  const int s = n + 1, i = node % s, j = node / s;
+  const bool interior = (i > 0 && i < n && j > 0 && j < n);
+  for (int k = 0; k < 2; ++k) {
+    const int row = 2 * node + k;
+    long long o = rp[row];
+    if (!interior) {
+      val[o] = 1.0;
+      continue;
+    }
+    for (int sl = 0; sl < 9; ++sl)
+      for (int m = 0; m < 2; ++m) val[o++] = Jst[(long long)(sl * 4 + k * 2 + m) * Nn + node];
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static double finish_sum(Ctx& c, const double* part, int nparts);
+
+void set_step_impl(Ctx& c, double dt, double t_new, const double* h, const double* A, const double* v_prev,
+                   const double* v_air, const double* v_ocean, const double* load) {
+  SI_CHECK(h && A && v_prev && v_air && v_ocean, SEAICE_EINVAL, "set_step: NULL input pointer");
+  SI_CHECK(dt > 0.0 && std::isfinite(dt), SEAICE_EINVAL, "set_step: dt must be positive");
+  c.dt = dt;
+  c.t_new = t_new;
+  c.ph.dt = dt;
+  cudaStream_t s = c.s;
+  SI_CUDA(cudaMemsetAsync(c.flag.get(), 0, sizeof(int) * 4, s));
+  SI_CUDA(cudaMemcpyAsync(c.vprev.get(), v_prev, sizeof(double) * c.N, cudaMemcpyDeviceToDevice, s));
+  SI_CUDA(cudaMemcpyAsync(c.vair.get(), v_air, sizeof(double) * c.N, cudaMemcpyDeviceToDevice, s));
+  SI_CUDA(cudaMemcpyAsync(c.vocean.get(), v_ocean, sizeof(double) * c.N, cudaMemcpyDeviceToDevice, s));
+  k_cell_setup<<<grid_for(c.Nc), kThreads, 0, s>>>(c.Nc, c.ph, h, A, c.P.get(), c.rhoh.get(), c.flag.get());
+  SI_LAUNCHED(c);
+  for (int k = 0; k < 3; ++k) {
+    const double* x = k == 0 ? c.vprev.get() : k == 1 ? c.vair.get() : c.vocean.get();
+    k_check_finite<<<grid_for(c.N), kThreads, 0, s>>>(c.N, x, c.flag.get(), 2);
+    SI_LAUNCHED(c);
+  }
+  c.have_load = load != nullptr;
+  if (load) {
+    c.load.ensure(c.al, c.N);
+    SI_CUDA(cudaMemcpyAsync(c.load.get(), load, sizeof(double) * c.N, cudaMemcpyDeviceToDevice, s));
+    k_check_finite<<<grid_for(c.N), kThreads, 0, s>>>(c.N, c.load.get(), c.flag.get(), 2);
+    SI_LAUNCHED(c);
+  }
+  k_force<<<grid_for(c.Nn), kThreads, 0, s>>>(c.ph, c.Nn, c.vprev.get(), c.vocean.get(), c.vair.get(), c.rhoh.get(),
+                                               c.have_load ? c.load.get() : nullptr, c.F.get());
+  SI_LAUNCHED(c);
+  k_pi_init<<<grid_for(c.Nc), kThreads, 0, s>>>(c.ph, c.Nc, c.vprev.get(), c.pi.get());
+  SI_LAUNCHED(c);
+  int flag = 0;
+  SI_CUDA(cudaMemcpyAsync(c.hbuf, c.flag.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  SI_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(&flag, c.hbuf, sizeof(int));
+  c.step_set = false;
+  SI_CHECK(!(flag & 1), SEAICE_EINVAL, "set_step: A outside [0,1], h < 0 or non-finite cell field");
+  SI_CHECK(!(flag & 2), SEAICE_EINVAL, "set_step: non-finite nodal input");
+  c.step_set = true;
+  c.assembled = false;
+  c.amg_ready = false;
+  c.have_r0 = false;
+}
+
+template <int KIND, bool JAC>
+static void launch_assemble(Ctx& c, const double* v, const double* pi, double* R) {
+  const int g = grid_for(c.Nn, 128);
+  c.part.ensure(c.al, g + 64);
+  k_assemble<KIND, JAC><<<g, 128, 0, c.s>>>(c.ph, c.Nn, v, pi, c.P.get(), c.rhoh.get(), c.vocean.get(), c.F.get(),
+                                             c.Jst.get(), R, c.part.get());
+  SI_LAUNCHED(c);
+}
+
+void assemble_impl(Ctx& c, const double* v, const double* pi, bool jac, double* r_out, double* norm_host) {
+  SI_CHECK(c.step_set, SEAICE_ESTATE, "assemble/residual called before set_step");
+  SI_CHECK(v, SEAICE_EINVAL, "NULL velocity");
+  const double* pp = pi ? pi : c.pi.get();
+  double* R = c.R.get();
+  const int kind = c.p.jacobian;
+  if (!jac) {
+    launch_assemble<SEAICE_JAC_PICARD, false>(c, v, pp, R);
+  } else if (kind == SEAICE_JAC_SV) {
+    launch_assemble<SEAICE_JAC_SV, true>(c, v, pp, R);
+  } else if (kind == SEAICE_JAC_STD) {
+    launch_assemble<SEAICE_JAC_STD, true>(c, v, pp, R);
+  } else {
+    launch_assemble<SEAICE_JAC_PICARD, true>(c, v, pp, R);
+  }
+  if (r_out) {
+    SI_CUDA(cudaMemcpyAsync(r_out, R, sizeof(double) * c.N, cudaMemcpyDeviceToDevice, c.s));
+  }
+  const double n2 = finish_sum(c, c.part.get(), grid_for(c.Nn, 128));
+  c.last_res_norm = std::sqrt(n2);
+  if (norm_host) *norm_host = c.last_res_norm;
+  if (jac) {
+    c.assembled = true;
+    c.amg_ready = false;
+  }
+}
+
+// sum of partials -> host (one block, fixed order)
+__global__ void k_sum_partials(const double* __restrict__ part, int nparts, int ncols, long long stride,
+                               double* __restrict__ out) {
+  __shared__ double sh[32];
+  for (int col = 0; col < ncols; ++col) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += part[col * stride + i];
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) out[col] = s;
+    __syncthreads();
+  }
+}
+
+static double finish_sum(Ctx& c, const double* part, int nparts) {
+  k_sum_partials<<<1, 1024, 0, c.s>>>(part, nparts, 1, 0, c.scal.get());
+  SI_LAUNCHED(c);
+  SI_CUDA(cudaMemcpyAsync(c.hbuf, c.scal.get(), sizeof(double), cudaMemcpyDeviceToHost, c.s));
+  SI_CUDA(cudaStreamSynchronize(c.s));
+  return c.hbuf[0];
+}
+
+void delta_energy_impl(Ctx& c, const double* v, const double* vt, const double* alphas, int count, double* out) {
+  SI_CHECK(c.step_set, SEAICE_ESTATE, "delta_energy before set_step");
+  SI_CHECK(count >= 1 && count <= 32, SEAICE_EINVAL, "delta_energy: 1 <= count <= 32");
+  const int g = grid_for(c.Nc, 128);
+  c.part.ensure(c.al, (size_t)g * kMaxAlpha + 64);
+  for (int k0 = 0; k0 < count; k0 += kMaxAlpha) {
+    const int cnt = std::min(kMaxAlpha, count - k0);
+    std::memcpy(c.hbuf, alphas + k0, sizeof(double) * cnt);
+    SI_CUDA(cudaMemcpyAsync(c.scal.get() + 32, c.hbuf, sizeof(double) * cnt, cudaMemcpyHostToDevice, c.s));
+    k_delta_energy<<<g, 128, 0, c.s>>>(c.ph, c.Nc, v, vt, c.vprev.get(), c.vocean.get(), c.vair.get(), c.P.get(),
+                                        c.rhoh.get(), c.scal.get() + 32, cnt, c.part.get());
+    SI_LAUNCHED(c);
+    k_sum_partials<<<1, 1024, 0, c.s>>>(c.part.get(), g, cnt, g, c.scal.get());
+    SI_LAUNCHED(c);
+    SI_CUDA(cudaMemcpyAsync(c.hbuf, c.scal.get(), sizeof(double) * cnt, cudaMemcpyDeviceToHost, c.s));
+    SI_CUDA(cudaStreamSynchronize(c.s));
+    for (int k = 0; k < cnt; ++k) out[k0 + k] = c.hbuf[k];
+  }
+  if (c.have_load) {
+    const double lv = dot(c, c.load.get(), vt, c.N);
+    for (int k = 0; k < count; ++k) out[k] -= alphas[k] * lv;
+  }
+}
+
+void pi_tilde_impl(Ctx& c, const double* v, const double* pi, const double* vt, double* out, double alpha,
+                   bool update) {
+  SI_CHECK(c.step_set, SEAICE_ESTATE, "pi_tilde before set_step");
+  k_pi_tilde<<<grid_for(c.Nc), kThreads, 0, c.s>>>(c.ph, c.Nc, v, pi, vt, out, alpha, update ? 1 : 0,
+                                                    c.p.project_pi);
+  SI_LAUNCHED(c);
+}
+
+void build_csr_view(Ctx& c, seaice_csr* out) {
+  if (!c.csr_pattern) {
+    const int n = c.n, s = n + 1;
+    std::vector<int> rp(c.N + 1), ci;
+    long long nnz = 0;
+    for (int node = 0; node < c.Nn; ++node) {
+      const int i = node % s, j = node / s;
+      const bool interior = (i > 0 && i < n && j > 0 && j < n);
+      for (int k = 0; k < 2; ++k) {
+        rp[2 * node + k] = (int)nnz;
+        nnz += interior ? 18 : 1;
+      }
+    }
+    rp[c.N] = (int)nnz;
+    ci.resize(nnz);
+    for (int node = 0; node < c.Nn; ++node) {
+      const int i = node % s, j = node / s;
+      const bool interior = (i > 0 && i < n && j > 0 && j < n);
+      for (int k = 0; k < 2; ++k) {
+        long long o = rp[2 * node + k];
+        if (!interior) {
+          ci[o] = 2 * node + k;
+          continue;
+        }
+        for (int sl = 0; sl < 9; ++sl) {
+          const int nb = (j + sl / 3 - 1) * s + (i + sl % 3 - 1);
+          for (int m = 0; m < 2; ++m) ci[o++] = 2 * nb + m;
+        }
+      }
+    }
+    c.csr_rp.ensure(c.al, c.N + 1);
+    c.csr_ci.ensure(c.al, nnz);
+    c.csr_val.ensure(c.al, nnz);
+    SI_CUDA(cudaMemcpyAsync(c.csr_rp.get(), rp.data(), sizeof(int) * (c.N + 1), cudaMemcpyHostToDevice, c.s));
+    SI_CUDA(cudaMemcpyAsync(c.csr_ci.get(), ci.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice, c.s));
+    SI_CUDA(cudaStreamSynchronize(c.s));
+    c.csr_nnz = nnz;
+    c.csr_pattern = true;
+  }
+  k_csr_values<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), c.csr_rp.get(), c.csr_val.get());
+  SI_LAUNCHED(c);
+  out->nrows = c.N;
+  out->ncols = c.N;
+  out->nnz = c.csr_nnz;
+  out->row_ptr = c.csr_rp.get();
+  out->col_idx = c.csr_ci.get();
+  out->val = c.csr_val.get();
+}
+
+}  // namespace seaice

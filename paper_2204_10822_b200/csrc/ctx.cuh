@@ -1,0 +1,127 @@
+// ctx.cuh — the library context and the host-side entry points of every kernel family.
+#pragma once
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "fem.cuh"
+
+namespace seaice {
+
+// One level of the AMG hierarchy.  Matrices are
+// block-CSR: A_l has b x b blocks (b = 2 on the finest level, 3 below), P_l has
+// b x 3 blocks, R_l = P_l^T has 3 x b blocks.
+struct Level {
+  int nb = 0, b = 0;          // block rows, block size
+  long long nnzb = 0;
+  DBuf<int> rp, ci;
+  DBuf<double> val;
+  DBuf<double> dinv;          // inverse diagonal blocks [nb][b*b]
+  double lmax = 0.0;          // power-iteration estimate of lambda_max(D^-1 A)
+  // transfer to the next level
+  int nbc = 0;                // coarse block rows
+  long long Pnnzb = 0, Rnnzb = 0;
+  DBuf<int> Prp, Pci, Rrp, Rci;
+  DBuf<double> Pval, Rval;
+  DBuf<int> agg;              // aggregate id per block row (-1: isolated, zero P row)
+  DBuf<double> B;             // near-nullspace rows [nb*b][3]
+  // V-cycle work vectors (length nb*b)
+  DBuf<double> x, rhs, r, d, d2, z;
+};
+
+struct Ctx {
+  seaice_params p{};
+  Allocator al;
+  cudaStream_t s = nullptr;
+  int n = 0, Nn = 0, N = 0, Nc = 0;
+  double dx = 0.0;
+  Phys ph{};
+  std::string err;
+  long long launches = 0;
+
+  // per-step state
+  bool step_set = false, assembled = false, amg_ready = false;
+  double dt = 0.0, t_new = 0.0;
+  DBuf<double> P, rhoh, F, vprev, vair, vocean, pi, vwork, load;
+  bool have_load = false;
+  DBuf<int> flag;  // validation / misc device flags
+
+  // finest-level Jacobian: 3x3 node stencil of 2x2 blocks, slot-major SoA
+  //   Jst[(s*4 + k*2 + m)*Nn + node], s = (dj+1)*3 + (di+1)
+  DBuf<double> Jst;
+  DBuf<double> R;  // residual of the last assemble
+  double last_res_norm = 0.0;
+  // scalar CSR view (built on demand)
+  DBuf<int> csr_rp, csr_ci;
+  DBuf<double> csr_val;
+  bool csr_pattern = false;
+  long long csr_nnz = 0;
+
+  // reductions
+  DBuf<double> part, scal;
+  double* hbuf = nullptr;  // pinned host scratch (64 doubles)
+
+  // Newton
+  bool have_r0 = false;
+  double r0 = 0.0;
+  DBuf<double> vt, pit;
+
+  // Krylov
+  DBuf<double> V, Z, w, xk, rk;
+
+  // AMG
+  std::vector<Level> lv;
+  DBuf<double> cinv;  // dense coarse inverse
+  int cn = 0;         // coarse DOFs
+  double op_complexity = 0.0;
+  DBuf<int> iwork;
+  DBuf<double> dwork;
+  DBuf<long long> lwork;
+
+  // staging buffers of the host-pointer entry point
+  DBuf<double> st_h, st_A, st_vp, st_va, st_vo, st_v;
+
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+inline void count_launch(Ctx& c, int k = 1) { c.launches += k; }
+#define SI_LAUNCHED(c) \
+  do {                 \
+    SI_CUDA(cudaGetLastError()); \
+    (c).launches++;    \
+  } while (0)
+
+// assembly.cu
+void set_step_impl(Ctx& c, double dt, double t_new, const double* h, const double* A, const double* v_prev,
+                   const double* v_air, const double* v_ocean, const double* load);
+void assemble_impl(Ctx& c, const double* v, const double* pi, bool jacobian, double* r_out, double* norm_host);
+void build_csr_view(Ctx& c, seaice_csr* out);
+void delta_energy_impl(Ctx& c, const double* v, const double* vt, const double* alphas, int count, double* out);
+void pi_tilde_impl(Ctx& c, const double* v, const double* pi, const double* vt, double* out, double alpha,
+                   bool update_in_place);
+
+// linalg.cu
+void stencil_spmv(Ctx& c, const double* x, double* y);
+void bsr_spmv(Ctx& c, const Level& L, const double* x, double* y);
+double dot(Ctx& c, const double* a, const double* b, long long n);
+double norm2(Ctx& c, const double* a, long long n);
+void axpy(Ctx& c, double a, const double* x, double* y, long long n);   // y += a x
+void scal_copy(Ctx& c, double a, const double* x, double* y, long long n);  // y = a x
+void xpby(Ctx& c, const double* x, double b, double* y, long long n);   // y = x + b y
+void fill(Ctx& c, double* y, double v, long long n);
+void copy(Ctx& c, double* dst, const double* src, long long n);
+// FGMRES helpers: h[0..j] = V[0..j]^T w ; w -= V h, return ||w||
+void multidot(Ctx& c, const double* V, long long ld, int k, const double* w, long long n, double* h_host);
+double multi_axpy_norm(Ctx& c, const double* V, long long ld, int k, const double* h_host, double* w, long long n);
+void multi_axpy(Ctx& c, const double* Z, long long ld, int k, const double* y_host, double* x, long long n);
+
+// krylov.cu
+int fgmres_impl(Ctx& c, const double* b, double* x, seaice_krylov_stats* st);
+void precond_apply(Ctx& c, const double* r, double* z);
+
+// amg.cu
+void amg_setup_impl(Ctx& c);
+void amg_vcycle(Ctx& c, const double* r, double* z);
+void amg_free(Ctx& c);
+
+}  // namespace seaice

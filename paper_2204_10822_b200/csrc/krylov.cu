@@ -1,0 +1,125 @@
+// krylov.cu — right-preconditioned FGMRES(m) driven from the host.
+// Definition shared with oracle/krylov.py (as a definition, not code): x0 = 0,
+// classical Gram-Schmidt in one pass, Givens rotations, stop when the estimate
+// |g_{j+1}| <= rtol ||b||, explicit residual at every restart.
+#include <cmath>
+#include <vector>
+
+#include "ctx.cuh"
+
+namespace seaice {
+
+static void apply_A(Ctx& c, const double* x, double* y) { stencil_spmv(c, x, y); }
+
+__global__ void k_point_jacobi(int Nn, const double* __restrict__ J, const double* __restrict__ r,
+                               double* __restrict__ z) {
+  const int node = blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= Nn) return;
+  // diagonal entries of the centre block: slot 4, (0,0) and (1,1)
+  z[2 * node] = r[2 * node] / J[16LL * Nn + node];
+  z[2 * node + 1] = r[2 * node + 1] / J[19LL * Nn + node];
+}
+
+void precond_apply(Ctx& c, const double* r, double* z) {
+  switch (c.p.precond) {
+    case SEAICE_PC_NONE:
+      copy(c, z, r, c.N);
+      break;
+    case SEAICE_PC_JACOBI:
+      k_point_jacobi<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.Nn, c.Jst.get(), r, z);
+      SI_LAUNCHED(c);
+      break;
+    default:
+      SI_CHECK(c.amg_ready, SEAICE_ESTATE, "AMG preconditioner requested before seaice_amg_setup");
+      amg_vcycle(c, r, z);
+  }
+}
+
+int fgmres_impl(Ctx& c, const double* b, double* x, seaice_krylov_stats* st) {
+  SI_CHECK(c.assembled, SEAICE_ESTATE, "fgmres before assemble_jacobian");
+  const int m = c.p.restart;
+  const long long N = c.N;
+  c.V.ensure(c.al, (size_t)(m + 1) * N);
+  c.Z.ensure(c.al, (size_t)m * N);
+  c.w.ensure(c.al, N);
+  c.rk.ensure(c.al, N);
+  double* V = c.V.get();
+  double* Z = c.Z.get();
+  double* w = c.w.get();
+  fill(c, x, 0.0, N);
+  const double bnorm = norm2(c, b, N);
+  seaice_krylov_stats S{0, 0, 1, 0.0, 0.0};
+  if (bnorm == 0.0) {
+    if (st) *st = S;
+    return SEAICE_OK;
+  }
+  SI_CHECK(std::isfinite(bnorm), SEAICE_ENONFINITE, "fgmres: non-finite right-hand side");
+  const double tol = c.p.krylov_rtol * bnorm;
+  std::vector<double> H((m + 1) * m), cs(m), sn(m), g(m + 1), h(m + 2), y(m);
+  double beta = bnorm;
+  const double* r = b;
+  int its = 0;
+  double est = bnorm;
+  bool converged = false;
+  while (true) {
+    std::fill(H.begin(), H.end(), 0.0);
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    scal_copy(c, 1.0 / beta, r, V, N);
+    int jd = 0;
+    for (int j = 0; j < m; ++j) {
+      double* vj = V + (long long)j * N;
+      double* zj = Z + (long long)j * N;
+      precond_apply(c, vj, zj);
+      apply_A(c, zj, w);
+      multidot(c, V, N, j + 1, w, N, h.data());
+      const double hn = multi_axpy_norm(c, V, N, j + 1, h.data(), w, N);
+      SI_CHECK(std::isfinite(hn), SEAICE_ENONFINITE, "fgmres: non-finite Arnoldi vector");
+      for (int i = 0; i <= j; ++i) H[i * m + j] = h[i];
+      H[(j + 1) * m + j] = hn;
+      if (hn > 0.0) scal_copy(c, 1.0 / hn, w, V + (long long)(j + 1) * N, N);
+      for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * H[i * m + j] + sn[i] * H[(i + 1) * m + j];
+        H[(i + 1) * m + j] = -sn[i] * H[i * m + j] + cs[i] * H[(i + 1) * m + j];
+        H[i * m + j] = t;
+      }
+      const double den = std::hypot(H[j * m + j], H[(j + 1) * m + j]);
+      cs[j] = H[j * m + j] / den;
+      sn[j] = H[(j + 1) * m + j] / den;
+      H[j * m + j] = den;
+      H[(j + 1) * m + j] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      ++its;
+      jd = j + 1;
+      est = std::fabs(g[j + 1]);
+      if (est <= tol || hn == 0.0 || its >= c.p.krylov_maxit) break;
+    }
+    // y = H^-1 g (upper triangular), x += Z y
+    for (int i = jd - 1; i >= 0; --i) {
+      double t = g[i];
+      for (int k = i + 1; k < jd; ++k) t -= H[i * m + k] * y[k];
+      y[i] = t / H[i * m + i];
+    }
+    multi_axpy(c, Z, N, jd, y.data(), x, N);
+    // explicit residual r = b - A x
+    apply_A(c, x, c.rk.get());
+    xpby(c, b, -1.0, c.rk.get(), N);
+    beta = norm2(c, c.rk.get(), N);
+    r = c.rk.get();
+    S.relres_est = est / bnorm;
+    if (beta <= tol || est <= tol) {
+      converged = true;
+      break;
+    }
+    if (its >= c.p.krylov_maxit) break;
+    S.restarts++;
+  }
+  S.iters = its;
+  S.relres_true = beta / bnorm;
+  S.converged = converged ? 1 : 0;
+  if (st) *st = S;
+  return converged ? SEAICE_OK : SEAICE_NOT_CONVERGED;
+}
+
+}  // namespace seaice

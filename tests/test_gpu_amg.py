@@ -1,0 +1,159 @@
+"""GPU AMG (setup on the GPU + V-cycle) against oracle/amg.py (same definition, independent
+code) and against algebraic properties that hold at any size."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import amg as OA
+from oracle import krylov, newton
+from oracle import model as M
+from paper_2204_10822_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+PRM = wl.PhysParams()
+
+
+def make_ctx(n, **kw):
+    from paper_2204_10822_b200.seaice import SeaIce
+    return SeaIce(n, **kw)
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+def bsr_to_scipy(d):
+    v = np_(d["val"]).reshape(-1, d["br"], d["bc"])
+    return sp.bsr_matrix((v, np_(d["col_idx"]), np_(d["row_ptr"])),
+                         shape=(d["nbrows"] * d["br"], d["nbcols"] * d["bc"])).tocsr()
+
+
+def rows_close(A, B, tol):
+    D = (A - B).tocsr()
+    dm = abs(D).max(axis=1).toarray().ravel()
+    rm = np.maximum(abs(A).max(axis=1).toarray().ravel(), abs(B).max(axis=1).toarray().ravel())
+    return np.max(dm / np.maximum(rm, 1e-300))
+
+
+def newton_state(n, seed, iters):
+    """An sv-Newton iterate (v_l, pi_l) of the oracle after `iters` steps (direct solves)."""
+    _, inp = wl.custom_inputs(n, seed=seed)
+    pb = M.Problem(inp, PRM)
+    if iters == 0:
+        v = pb.v_prev.copy()
+        return inp, pb, v, pb.pi_consistent(v)
+    _, _, h = newton.solve_step(inp, PRM, maxit=iters, rtol=0.0, record_iterates=True)
+    v, pi = h["iterates"][iters]
+    return inp, pb, v, pi
+
+
+@pytest.mark.parametrize("n,it", [(32, 0), (32, 6), (64, 3)])
+def test_hierarchy_matches_oracle(n, it):
+    inp, pb, v, pi = newton_state(n, n, it)
+    J = pb.jacobian(v, pi, "sv")
+    H = OA.setup(J, pb)
+    ctx = make_ctx(n)
+    ctx.set_inputs(inp)
+    ctx.assemble_jacobian(v, pi.ravel(), want_csr=False)
+    nlev, oc = ctx.amg_setup()
+    assert nlev == len(H["levels"])
+    assert abs(oc - H["op_complexity"]) <= 0.02 * H["op_complexity"]  # explicit zeros differ slightly
+    for l in range(nlev):
+        A, P, agg = ctx.amg_level(l)
+        Ao = H["levels"][l]["A"]
+        assert rows_close(bsr_to_scipy(A), Ao, 1.0) <= 1e-11, l
+        if l < nlev - 1:
+            assert np.array_equal(agg, H["levels"][l]["agg"]), l
+            assert rows_close(bsr_to_scipy(P), H["levels"][l]["P"], 1.0) <= 1e-11, l
+
+
+def test_galerkin_and_transfer_properties():
+    """Algebra of the GPU hierarchy at a size the oracle AMG would be slow at: A_c = P^T A P
+    (recomputed with scipy from the GPU's own P and A), symmetry of A_c, aggregates valid."""
+    n = 128
+    inp, pb, v, pi = newton_state(n, 5, 0)
+    ctx = make_ctx(n)
+    ctx.set_inputs(inp)
+    v = wl.random_velocity(n, 3, amp=0.05)
+    pi = wl.random_pi(n, 4, max_norm=1.2)
+    ctx.assemble_jacobian(v, pi.ravel(), want_csr=False)
+    nlev, oc = ctx.amg_setup()
+    assert nlev >= 2 and 1.0 < oc < 4.0
+    for l in range(nlev - 1):
+        A, P, agg = ctx.amg_level(l)
+        Ac, _, _ = ctx.amg_level(l + 1)
+        As, Ps, Acs = bsr_to_scipy(A), bsr_to_scipy(P), bsr_to_scipy(Ac)
+        G = (Ps.T @ As @ Ps).tocsr()
+        d = G.diagonal()
+        G = G + sp.diags((d == 0).astype(float))
+        assert rows_close(Acs, G, 1.0) <= 1e-12
+        assert rows_close(Acs, Acs.T.tocsr(), 1.0) <= 1e-12
+        assert agg.min() >= -1 and agg.max() == P["nbcols"] - 1
+        assert len(np.unique(agg[agg >= 0])) == P["nbcols"]        # every aggregate non-empty
+
+
+def test_vcycle_parity_and_symmetry():
+    n = 48
+    inp, pb, v, pi = newton_state(n, 7, 4)
+    J = pb.jacobian(v, pi, "sv")
+    H = OA.setup(J, pb)
+    ctx = make_ctx(n)
+    ctx.set_inputs(inp)
+    ctx.assemble_jacobian(v, pi.ravel(), want_csr=False)
+    ctx.amg_setup()
+    r1 = wl.random_interior_vector(n, 1)
+    r2 = wl.random_interior_vector(n, 2)
+    z1 = np_(ctx.precond_apply(r1))
+    z2 = np_(ctx.precond_apply(r2))
+    zo = OA.vcycle(H, r1)
+    assert np.linalg.norm(z1 - zo) <= 1e-9 * np.linalg.norm(zo)
+    assert abs(z1 @ r2 - r1 @ z2) <= 1e-10 * abs(z1 @ r2)
+    # deterministic
+    assert np.array_equal(z1, np_(ctx.precond_apply(r1)))
+
+
+def test_single_level_is_exact_solve():
+    """N <= coarse_max_dof: the hierarchy is one dense level and M^-1 = J^-1."""
+    n = 12
+    inp, pb, v, pi = newton_state(n, 9, 0)
+    ctx = make_ctx(n)
+    ctx.set_inputs(inp)
+    v = wl.random_velocity(n, 3)
+    ctx.assemble_jacobian(v, pb.pi_consistent(v).ravel(), want_csr=False)
+    nlev, _ = ctx.amg_setup()
+    assert nlev == 1
+    J = pb.jacobian(v, pb.pi_consistent(v), "sv")
+    r = wl.random_interior_vector(n, 5)
+    z = np_(ctx.precond_apply(r))
+    assert np.linalg.norm(J @ z - r) <= 1e-10 * np.linalg.norm(r)
+
+
+@pytest.mark.parametrize("n,it", [(32, 0), (32, 5), (64, 8)])
+def test_amg_fgmres_counts_parity(n, it):
+    inp, pb, v, pi = newton_state(n, 11, it)
+    J = pb.jacobian(v, pi, "sv")
+    R = pb.residual(v)
+    H = OA.setup(J, pb)
+    xo, so = krylov.fgmres(lambda x: J @ x, R, lambda r: OA.vcycle(H, r), 30, 1e-8, 300)
+    ctx = make_ctx(n)
+    ctx.set_inputs(inp)
+    ctx.assemble_jacobian(v, pi.ravel(), want_csr=False)
+    ctx.amg_setup()
+    xg, sg, rc = ctx.fgmres(R)
+    assert abs(sg["iters"] - so["iters"]) <= max(1, 0.1 * so["iters"]), (sg, so)
+    xd = krylov.sparse_direct_solve(J, R)
+    assert np.linalg.norm(np_(xg) - xd) <= 1e-6 * np.linalg.norm(xd)
+
+
+def test_newton_amg_config1_parity():
+    """Config 1 implicit step with the product path (AMG-FGMRES): Newton count +-1 and
+    converged v to 1e-8 relative L2 vs the oracle with direct solves."""
+    cfg = wl.CONFIGS[1]
+    inp = wl.step_inputs(cfg, 0)
+    vo, _, ho = newton.solve_step(inp, PRM)
+    ctx = make_ctx(cfg.n, krylov_rtol=1e-10)
+    vg, st = ctx.solve_step(inp.dt, inp.t_new, inp.h, inp.A, inp.v_prev, inp.v_air, inp.v_ocean)
+    assert st["converged"] == 1
+    assert abs(st["newton_iters"] - ho["newton_iters"]) <= 1
+    assert np.linalg.norm(np_(vg) - vo) <= 1e-8 * np.linalg.norm(vo)

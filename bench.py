@@ -1,0 +1,348 @@
+"""bench.py — the B200 stress-velocity Newton-Krylov sea-ice step (BASELINE.json metric).
+
+A "step" is one implicit time step of the configured workload: seaice_set_step (a-1:
+ice strength, RHS, pi_0) followed by sv-Newton iterations (a-2..a-7: fused residual +
+Jacobian assembly, GPU AMG setup, AMG-FGMRES solve, energy backtracking, v/pi update) until
+||R|| <= 1e-8 ||R_0||.  Default workload: BASELINE.json configs[4] ("2048x2048 Q1 mesh,
+~8.4M unknowns, seed 3, moving cyclone") — the paper's largest problem.
+
+value = DOF * (FGMRES iterations) / s over the timed steps, summed over ranks (weak scaling:
+every rank solves an independent replica; the method has no data-path collective at this
+size).  s/timestep is reported beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+
+from paper_2204_10822_b200 import workloads as wl
+
+METRIC = "DOF*Krylov-iters/s"
+UNIT = "DOF*iter/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--params", default="{}", help="JSON overrides of seaice_params")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def oracle_sample(cfg, n_sample=256):
+    """One full sv-Newton iteration of the CPU oracle (assembly, AMG setup, AMG-FGMRES,
+    energy line search, update) on the workload's generator at mesh n_sample.
+    Returns (DOF * Krylov iterations, seconds, description)."""
+    from oracle import amg as OA
+    from oracle import krylov
+    from oracle.model import Problem
+    prm = wl.PhysParams()
+    scfg = wl.Config(cfg.name + f"_sample{n_sample}", n_sample, cfg.seed, 1, cfg.moving, cfg.kind, cfg.dt)
+    inp = wl.step_inputs(scfg, 0)
+    t0 = time.perf_counter()
+    pb = Problem(inp, prm)
+    v = pb.v_prev.copy()
+    pi = pb.pi_consistent(v)
+    R = pb.residual(v)
+    J = pb.jacobian(v, pi, "sv")
+    H = OA.setup(J, pb)
+    vt, st = krylov.fgmres(lambda x: J @ x, R, lambda r: OA.vcycle(H, r), 30, 1e-8, 300)
+    for k in range(21):
+        if pb.delta_energy(v, vt, 0.5 ** k) < 0:
+            break
+    pi = pi + 0.5 ** k * pb.pi_tilde(v, pi, vt)
+    v = v + 0.5 ** k * vt
+    dt_s = time.perf_counter() - t0
+    N = 2 * (n_sample + 1) ** 2
+    desc = (f"one full sv-Newton iteration of the CPU oracle (numpy/scipy, fp64) on {cfg.name}'s "
+            f"generator at n={n_sample} ({N} DOF, first iteration of implicit step 1): residual + "
+            f"Jacobian assembly, AMG setup, AMG-FGMRES(30) to 1e-8 ({st['iters']} its), line search, update")
+    return N * st["iters"], dt_s, desc
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    cfg = wl.CONFIGS[a.config]
+    cores = int(os.environ.get("OMP_NUM_THREADS", "0")) or os.cpu_count()
+    for _ in range(a.warmup):
+        oracle_sample(cfg)
+    units = 0.0
+    secs = 0.0
+    desc = ""
+    for _ in range(a.steps):
+        u, s, desc = oracle_sample(cfg)
+        units += u
+        secs += s
+    val = units / secs
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * secs / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "n": cfg.n, "sample_n": 256},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+BYTES_NOTE = {
+    "cheb0": "finest-level fused Chebyshev step: 9 stencil slots x 2x2 fp64 (288 B/node) + vector traffic per variant",
+}
+
+
+def run_ours(a, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2204_10822_b200.seaice import SeaIce
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = wl.CONFIGS[a.config]
+    n = cfg.n
+    ctx = SeaIce(n, **json.loads(a.params))
+    N, Nc = ctx.N, ctx.Nc
+    h_np, A_np = wl.ice_fields(cfg)
+    vo_np = wl.ocean_nodal(n)
+    total = a.warmup + a.steps
+    winds = [wl.wind_nodal(n, (s + 1) * cfg.dt, cfg.moving) for s in range(total)]
+    h = torch.tensor(h_np, device=dev)
+    A = torch.tensor(A_np, device=dev)
+    vo = torch.tensor(vo_np, device=dev)
+    va = [torch.tensor(w, device=dev) for w in winds]
+    v = torch.zeros(N, dtype=torch.float64, device=dev)
+    v_out = torch.zeros_like(v)
+    for s in range(a.warmup):
+        v_out, st = ctx.solve_step(cfg.dt, (s + 1) * cfg.dt, h, A, v, va[s], vo, v_out)
+        v, v_out = v_out, v
+    v_start = v.clone()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident timed region
+    stats = []
+    launches0 = ctx.launches
+    ctx.profile(True)
+    barrier()
+    with Clocks(local_rank) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for s in range(a.warmup, total):
+            v_out, st = ctx.solve_step(cfg.dt, (s + 1) * cfg.dt, h, A, v, va[s], vo, v_out)
+            v, v_out = v_out, v
+            stats.append(st)
+        e1.record()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    launches = ctx.launches - launches0
+    kry = sum(s["krylov_iters_total"] for s in stats)
+    units = float(N) * kry
+    t = torch.tensor([ms, units], dtype=torch.float64, device=dev)
+    if world > 1:
+        tm = t[:1].clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        tu = t[1:].clone()
+        dist.all_reduce(tu, op=dist.ReduceOp.SUM)
+        ms_max, units_all = float(tm.item()), float(tu.item())
+    else:
+        ms_max, units_all = ms, units
+    value = units_all / (ms_max / 1e3)
+
+    # ---- end-to-end through the host-buffer C-ABI call (same steps again)
+    e2e = None
+    if not a.no_e2e:
+        pin = lambda x: torch.tensor(x, dtype=torch.float64).pin_memory()
+        hh, AA, vvo = pin(h_np), pin(A_np), pin(vo_np)
+        vva = [pin(winds[s]) for s in range(a.warmup, total)]
+        vin = v_start.cpu().pin_memory()
+        vout_h = torch.zeros(N, dtype=torch.float64).pin_memory()
+        e2e_stats = []
+        barrier()
+        e0.record()
+        for k, s in enumerate(range(a.warmup, total)):
+            st = ctx.solve_step_host(cfg.dt, (s + 1) * cfg.dt, hh, AA, vin, vva[k], vvo, vout_h)
+            vin, vout_h = vout_h, vin
+            e2e_stats.append(st)
+        e1.record()
+        barrier()
+        ms_e = e0.elapsed_time(e1)
+        kry_e = sum(s["krylov_iters_total"] for s in e2e_stats)
+        te = torch.tensor([ms_e, float(N) * kry_e], dtype=torch.float64, device=dev)
+        if world > 1:
+            x = te[:1].clone()
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+            y = te[1:].clone()
+            dist.all_reduce(y, op=dist.ReduceOp.SUM)
+            ms_e, u_e = float(x.item()), float(y.item())
+        else:
+            u_e = float(N) * kry_e
+        e2e = {"value": u_e / (ms_e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * (2 * Nc + 3 * N),
+               "d2h_bytes_per_step": 8 * N, "ms_per_step": ms_e / a.steps,
+               "s_per_timestep": ms_e / 1e3 / a.steps}
+
+    if rank != 0:
+        return
+    # ---- roofline of the dominant kernel class (algorithmic bytes / CUDA-event time)
+    peak, peak_src = peaks()
+    kern = {}
+    for name, d in prof.items():
+        if d["launches"] == 0 or d["ms"] <= 0:
+            continue
+        kern[name] = {"ms_total": round(d["ms"], 3), "launches": d["launches"],
+                      "us_per_launch": round(1e3 * d["ms"] / d["launches"], 2),
+                      "share_of_step": round(d["ms"] / ms, 4)}
+        if d.get("bytes"):
+            gbs = d["bytes"] / (d["ms"] / 1e3) / 1e9
+            kern[name].update({"alg_bytes_per_launch": d["bytes"] / d["launches"], "achieved_gbs": round(gbs, 1),
+                               "frac_of_peak": round(gbs / peak, 4)})
+    dom = max(kern, key=lambda k: kern[k]["ms_total"]) if kern else None
+    roof = None
+    if dom and "achieved_gbs" in kern[dom]:
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(dom)
+        roof = {"kernel": dom, "bound": "hbm", "achieved": kern[dom]["achieved_gbs"], "peak": peak,
+                "unit": "GB/s", "frac": kern[dom]["frac_of_peak"], "traffic": traffic, "peak_source": peak_src,
+                "bytes_per_launch": kern[dom]["alg_bytes_per_launch"],
+                "us_per_launch": kern[dom]["us_per_launch"]}
+    cpu = None
+    if not a.no_cpu_baseline:
+        try:
+            u, s, desc = oracle_sample(cfg)
+            cpu = {"value": u / s, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": desc,
+                   "seconds": round(s, 2)}
+        except Exception as ex:  # the baseline must never break the bench line
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {ex}"}
+    mem_live, mem_peak = ctx.memory()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "n": n, "dof": N, "seed": cfg.seed, "dt": cfg.dt,
+                   "steps_timed": [s + 1 for s in range(a.warmup, total)], "parallelism": f"replicas x{world}",
+                   "l2": "working set (J 1.2 GB + Krylov basis + AMG) far larger than the 126 MB L2; no flush",
+                   "newton_rtol": 1e-8, "krylov": "FGMRES(30) rtol 1e-8, AMG(MIS2-SA, Chebyshev-3)"},
+        "s_per_timestep": ms_max / 1e3 / a.steps,
+        "newton_iters": [s["newton_iters"] for s in stats],
+        "krylov_iters": [s["krylov_iters_total"] for s in stats],
+        "converged": [s["converged"] for s in stats],
+        "phase_ms": {k: round(sum(s[k] for s in stats) / a.steps, 2) for k in
+                     ("t_setup", "t_assemble", "t_amg", "t_krylov", "t_ls")},
+        "roofline": roof, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches, "clocks": clk.summary(),
+        "memory_gb": {"live": round(mem_live / 1e9, 2), "peak": round(mem_peak / 1e9, 2)},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(a, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

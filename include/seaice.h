@@ -208,6 +208,21 @@ int seaice_solve_step_host(seaice_ctx* ctx, double dt, double t_new, const doubl
 /* Number of kernels the library launched since create (evidence for bench.py). */
 int64_t seaice_launch_count(const seaice_ctx* ctx);
 
+/* Per-kernel-class timing with CUDA events recorded on the context stream around
+ * each launch.  Classes: 0 assembly (K1), 1 finest SpMV, 2 finest Chebyshev step,
+ * 3 coarse Chebyshev step, 4 finest residual+Dinv, 5 Krylov multi-dot, 6 multi-axpy+norm,
+ * 7 solution update, 8 line-search energy, 9 restriction/prolongation, 10 coarse solve,
+ * 11 coarse residual+Dinv, 12 dual update.  enable: resets the counters and turns the
+ * timing on (1) or off (0).  read: synchronizes, returns total milliseconds, launch
+ * counts and algorithmic bytes (DESIGN.md formulas) per class (arrays of
+ * SEAICE_PROF_CLASSES; any pointer may be NULL). */
+#define SEAICE_PROF_CLASSES 16
+int seaice_profile_enable(seaice_ctx* ctx, int32_t on);
+int seaice_profile_read(seaice_ctx* ctx, double* ms_host, int64_t* launches_host, double* alg_bytes_host);
+
+/* Bytes of device memory the context currently holds (and its peak). */
+int seaice_memory(const seaice_ctx* ctx, int64_t* live_bytes, int64_t* peak_bytes);
+
 #ifdef __cplusplus
 }
 #endif

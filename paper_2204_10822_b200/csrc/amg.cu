@@ -1178,6 +1178,7 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
   double* d2 = L.d2.get();
   const bool st = (l == 0);
   // r = b - A x ; d = Dinv r / th
+  prof_begin(c);
   if (st) {
     k_resid_dinv_stencil<<<grid_for(c.Nn), 256, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L.dinv.get(),
                                                           (const double2*)b, pre ? nullptr : (const double2*)x,
@@ -1190,6 +1191,12 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
                                                                L.dinv.get(), b, pre ? nullptr : x, r, d, 1.0 / k.th);
   }
   SI_LAUNCHED(c);
+  {
+    const double B = L.b;
+    double by = L.nb * (8.0 * B * 3 + 8.0 * B * B);  // b read, r write, d write, dinv
+    if (!pre) by += L.nnzb * (8.0 * B * B + (st ? 0.0 : 4.0)) + (st ? 0.0 : 4.0 * (L.nb + 1)) + 8.0 * B * L.nb;
+    prof_end(c, st ? PC_RESID0 : PC_RESIDC, by);
+  }
   for (int it = 0; it < m; ++it) {
     const bool last = (it == m - 1);
     const int want_r = (!last || pre) ? 1 : 0;
@@ -1197,6 +1204,7 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
     const int first = (pre && it == 0) ? 1 : 0;
     const double rho_new = 1.0 / (2.0 * k.sg - rho);
     const double c1 = rho_new * rho, c2 = 2.0 * rho_new / k.de;
+    prof_begin(c);
     if (st) {
       k_cheb_stencil<<<grid_for(c.Nn), 256, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L.dinv.get(), (const double2*)d,
                                                      (double2*)r, (double2*)x, (double2*)d2, c1, c2, first, want_r,
@@ -1209,6 +1217,13 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
                                                            r, x, d2, c1, c2, first, want_r, want_d);
     }
     SI_LAUNCHED(c);
+    {
+      const double B = L.b;
+      double by = L.nb * 8.0 * B * (first ? 2.0 : 3.0);  // d read, x (read +) write
+      if (want_r) by += L.nnzb * (8.0 * B * B + (st ? 0.0 : 4.0)) + (st ? 0.0 : 4.0 * (L.nb + 1)) + 16.0 * B * L.nb;
+      if (want_d) by += L.nb * (8.0 * B * B + 8.0 * B);
+      prof_end(c, st ? PC_CHEB0 : PC_CHEBC, by);
+    }
     rho = rho_new;
     std::swap(d, d2);
   }
@@ -1217,16 +1232,21 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
 static void vcycle_level(Ctx& c, int l, const double* b, double* x) {
   Level& L = c.lv[l];
   if (l + 1 == (int)c.lv.size()) {
+    prof_begin(c);
     k_dense_gemv<<<grid_for((long long)c.cn * 32, 256), 256, 0, c.s>>>(c.cn, c.cinv.get(), b, x);
     SI_LAUNCHED(c);
+    prof_end(c, PC_COARSE, 8.0 * c.cn * c.cn + 16.0 * c.cn);
     return;
   }
   smooth(c, l, b, x, true);
   Level& Lc = c.lv[l + 1];
   // r_c = R r
+  prof_begin(c);
   bsr_apply(c, L.nbc, 3, L.b, L.Rrp.get(), L.Rci.get(), L.Rval.get(), L.r.get(), Lc.rhs.get());
+  prof_end(c, PC_TRANSFER, L.Rnnzb * (24.0 * L.b + 4.0) + 4.0 * (L.nbc + 1) + 8.0 * L.b * L.nb + 24.0 * L.nbc);
   vcycle_level(c, l + 1, Lc.rhs.get(), Lc.x.get());
   // x += P e_c
+  prof_begin(c);
   if (L.b == 2)
     k_bsr_spmv_add<2, 3><<<grid_for(L.nb), kThreads, 0, c.s>>>(L.nb, L.Prp.get(), L.Pci.get(), L.Pval.get(),
                                                                Lc.x.get(), x);
@@ -1234,6 +1254,7 @@ static void vcycle_level(Ctx& c, int l, const double* b, double* x) {
     k_bsr_spmv_add<3, 3><<<grid_for(L.nb), kThreads, 0, c.s>>>(L.nb, L.Prp.get(), L.Pci.get(), L.Pval.get(),
                                                                Lc.x.get(), x);
   SI_LAUNCHED(c);
+  prof_end(c, PC_TRANSFER, L.Pnnzb * (24.0 * L.b + 4.0) + 4.0 * (L.nb + 1) + 16.0 * L.b * L.nb + 24.0 * L.nbc);
   smooth(c, l, b, x, false);
 }
 

@@ -264,6 +264,8 @@ int seaice_destroy(seaice_ctx* h) {
   c.iwork.free_();
   c.lwork.free_();
   for (auto* b : {&c.st_h, &c.st_A, &c.st_vp, &c.st_va, &c.st_vo, &c.st_v}) b->free_();
+  prof_harvest(c, true);
+  for (auto e : c.prof.free_ev) cudaEventDestroy(e);
   if (c.hbuf) cudaFreeHost(c.hbuf);
   if (c.ev0) cudaEventDestroy(c.ev0);
   if (c.ev1) cudaEventDestroy(c.ev1);
@@ -429,5 +431,39 @@ int seaice_solve_step_host(seaice_ctx* h, double dt, double t_new, const double*
 }
 
 int64_t seaice_launch_count(const seaice_ctx* h) { return h ? (int64_t)h->c.launches : 0; }
+
+int seaice_profile_enable(seaice_ctx* h, int32_t on) {
+  API_BEGIN(h)
+  SI_CUDA(cudaStreamSynchronize(c.s));
+  prof_harvest(c, true);
+  for (int k = 0; k < PC_NCLASS; ++k) {
+    c.prof.ms[k] = 0.0;
+    c.prof.cnt[k] = 0;
+    c.prof.bytes[k] = 0.0;
+  }
+  c.prof.on = on != 0;
+  return SEAICE_OK;
+  API_END
+}
+
+int seaice_profile_read(seaice_ctx* h, double* ms, int64_t* cnt, double* bytes) {
+  API_BEGIN(h)
+  SI_CUDA(cudaStreamSynchronize(c.s));
+  prof_harvest(c, true);
+  for (int k = 0; k < SEAICE_PROF_CLASSES; ++k) {
+    if (ms) ms[k] = k < PC_NCLASS ? c.prof.ms[k] : 0.0;
+    if (cnt) cnt[k] = k < PC_NCLASS ? c.prof.cnt[k] : 0;
+    if (bytes) bytes[k] = k < PC_NCLASS ? c.prof.bytes[k] : 0.0;
+  }
+  return SEAICE_OK;
+  API_END
+}
+
+int seaice_memory(const seaice_ctx* h, int64_t* live, int64_t* peak) {
+  if (!h) return SEAICE_EINVAL;
+  if (live) *live = (int64_t)h->c.al.live_bytes;
+  if (peak) *peak = (int64_t)h->c.al.peak_bytes;
+  return SEAICE_OK;
+}
 
 }  // extern "C"

@@ -491,9 +491,11 @@ template <int KIND, bool JAC>
 static void launch_assemble(Ctx& c, const double* v, const double* pi, double* R) {
   const int g = grid_for(c.Nn, 128);
   c.part.ensure(c.al, g + 64);
+  prof_begin(c);
   k_assemble<KIND, JAC><<<g, 128, 0, c.s>>>(c.ph, c.Nn, v, pi, c.P.get(), c.rhoh.get(), c.vocean.get(), c.F.get(),
                                              c.Jst.get(), R, c.part.get());
   SI_LAUNCHED(c);
+  prof_end(c, PC_ASSEMBLE, JAC ? 352.0 * c.Nn + 112.0 * c.Nc : 64.0 * c.Nn + 16.0 * c.Nc);
 }
 
 void assemble_impl(Ctx& c, const double* v, const double* pi, bool jac, double* r_out, double* norm_host) {
@@ -553,9 +555,11 @@ void delta_energy_impl(Ctx& c, const double* v, const double* vt, const double* 
     const int cnt = std::min(kMaxAlpha, count - k0);
     std::memcpy(c.hbuf, alphas + k0, sizeof(double) * cnt);
     SI_CUDA(cudaMemcpyAsync(c.scal.get() + 32, c.hbuf, sizeof(double) * cnt, cudaMemcpyHostToDevice, c.s));
+    prof_begin(c);
     k_delta_energy<<<g, 128, 0, c.s>>>(c.ph, c.Nc, v, vt, c.vprev.get(), c.vocean.get(), c.vair.get(), c.P.get(),
                                         c.rhoh.get(), c.scal.get() + 32, cnt, c.part.get());
     SI_LAUNCHED(c);
+    prof_end(c, PC_DENERGY, 80.0 * c.Nn + 16.0 * c.Nc);
     k_sum_partials<<<1, 1024, 0, c.s>>>(c.part.get(), g, cnt, g, c.scal.get());
     SI_LAUNCHED(c);
     SI_CUDA(cudaMemcpyAsync(c.hbuf, c.scal.get(), sizeof(double) * cnt, cudaMemcpyDeviceToHost, c.s));
@@ -571,9 +575,11 @@ void delta_energy_impl(Ctx& c, const double* v, const double* vt, const double* 
 void pi_tilde_impl(Ctx& c, const double* v, const double* pi, const double* vt, double* out, double alpha,
                    bool update) {
   SI_CHECK(c.step_set, SEAICE_ESTATE, "pi_tilde before set_step");
+  prof_begin(c);
   k_pi_tilde<<<grid_for(c.Nc), kThreads, 0, c.s>>>(c.ph, c.Nc, v, pi, vt, out, alpha, update ? 1 : 0,
                                                     c.p.project_pi);
   SI_LAUNCHED(c);
+  prof_end(c, PC_PIUPD, 32.0 * c.Nn + 192.0 * c.Nc);
 }
 
 void build_csr_view(Ctx& c, seaice_csr* out) {

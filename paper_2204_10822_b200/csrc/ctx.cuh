@@ -29,8 +29,42 @@ struct Level {
   DBuf<double> x, rhs, r, d, d2, z;
 };
 
+// Per-kernel-class CUDA-event timing (seaice_profile_enable/read): event pairs are
+// recorded on the context stream around the launches of one class and harvested
+// at host synchronisation points.
+enum ProfClass {
+  PC_ASSEMBLE = 0,  // K1 fused residual + Jacobian
+  PC_SPMV0 = 1,     // K3 finest stencil SpMV (FGMRES operator)
+  PC_CHEB0 = 2,     // K4 Chebyshev step, finest level
+  PC_CHEBC = 3,     // K4 Chebyshev step, coarse levels
+  PC_RESID0 = 4,    // residual + Dinv, finest level
+  PC_MDOT = 5,      // K7 multi-dot (CGS projections)
+  PC_MAXPY_NORM = 6,// K8 multi-axpy + norm
+  PC_MAXPY = 7,     // K10 solution update
+  PC_DENERGY = 8,   // K11 line-search energy differences
+  PC_TRANSFER = 9,  // K5 restriction / prolongation
+  PC_COARSE = 10,   // K6 dense coarse solve
+  PC_RESIDC = 11,   // residual + Dinv, coarse levels
+  PC_PIUPD = 12,    // K12 dual update
+  PC_NCLASS = 16
+};
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> free_ev;
+  struct Rec {
+    int k;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> pending;
+  cudaEvent_t cur_a = nullptr;
+  double ms[PC_NCLASS] = {0};
+  long long cnt[PC_NCLASS] = {0};
+  double bytes[PC_NCLASS] = {0};  // algorithmic bytes of the launches recorded
+};
+
 struct Ctx {
   seaice_params p{};
+  Prof prof;
   Allocator al;
   cudaStream_t s = nullptr;
   int n = 0, Nn = 0, N = 0, Nc = 0;
@@ -85,6 +119,52 @@ struct Ctx {
 };
 
 inline void count_launch(Ctx& c, int k = 1) { c.launches += k; }
+
+inline void prof_harvest(Ctx& c, bool wait) {
+  auto& P = c.prof;
+  size_t keep = 0;
+  for (size_t i = 0; i < P.pending.size(); ++i) {
+    auto& r = P.pending[i];
+    if (wait) cudaEventSynchronize(r.b);
+    if (cudaEventQuery(r.b) == cudaSuccess) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, r.a, r.b);
+      P.ms[r.k] += t;
+      P.cnt[r.k] += 1;
+      P.free_ev.push_back(r.a);
+      P.free_ev.push_back(r.b);
+    } else {
+      P.pending[keep++] = r;
+    }
+  }
+  P.pending.resize(keep);
+}
+inline cudaEvent_t prof_event(Ctx& c) {
+  auto& P = c.prof;
+  if (P.free_ev.empty()) {
+    if (P.pending.size() > 4096) prof_harvest(c, true);
+    if (P.free_ev.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+  }
+  cudaEvent_t e = P.free_ev.back();
+  P.free_ev.pop_back();
+  return e;
+}
+inline void prof_begin(Ctx& c) {
+  if (!c.prof.on) return;
+  c.prof.cur_a = prof_event(c);
+  cudaEventRecord(c.prof.cur_a, c.s);
+}
+inline void prof_end(Ctx& c, int k, double bytes = 0.0) {
+  if (!c.prof.on) return;
+  c.prof.bytes[k] += bytes;
+  cudaEvent_t b = prof_event(c);
+  cudaEventRecord(b, c.s);
+  c.prof.pending.push_back({k, c.prof.cur_a, b});
+}
 #define SI_LAUNCHED(c) \
   do {                 \
     SI_CUDA(cudaGetLastError()); \

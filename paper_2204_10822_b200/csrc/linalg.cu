@@ -37,9 +37,11 @@ __global__ void __launch_bounds__(256) k_stencil_spmv(int n, int Nn, const doubl
 }
 
 void stencil_spmv(Ctx& c, const double* x, double* y) {
+  prof_begin(c);
   k_stencil_spmv<<<grid_for(c.Nn), 256, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), reinterpret_cast<const double2*>(x),
                                                   reinterpret_cast<double2*>(y));
   SI_LAUNCHED(c);
+  prof_end(c, PC_SPMV0, 320.0 * c.Nn);
 }
 
 // ------------------------------------------------------------------ BSR SpMV
@@ -193,10 +195,12 @@ __global__ void __launch_bounds__(256) k_multidot(long long n, const double* __r
 void multidot(Ctx& c, const double* V, long long ld, int k, const double* w, long long n, double* h_host) {
   const int g = red_grid(n);
   c.part.ensure(c.al, (size_t)g * (k + 8));
+  prof_begin(c);
   for (int k0 = 0; k0 < k; k0 += 8) {
     k_multidot<8><<<g, 256, 0, c.s>>>(n, V, ld, k0, k, w, c.part.get());
     SI_LAUNCHED(c);
   }
+  prof_end(c, PC_MDOT, 8.0 * (k + 1) * n);
   finish_cols(c, g, k, h_host);
 }
 
@@ -225,8 +229,10 @@ double multi_axpy_norm(Ctx& c, const double* V, long long ld, int k, const doubl
   c.part.ensure(c.al, (size_t)g * 40);
   // pageable source: the runtime stages it before returning, so h_host may be reused at once
   SI_CUDA(cudaMemcpyAsync(c.scal.get() + 64, h_host, sizeof(double) * k, cudaMemcpyHostToDevice, c.s));
+  prof_begin(c);
   k_multi_axpy_norm<<<g, 256, 0, c.s>>>(n, V, ld, k, c.scal.get() + 64, w, c.part.get());
   SI_LAUNCHED(c);
+  prof_end(c, PC_MAXPY_NORM, 8.0 * (k + 2) * n);
   double r;
   finish_cols(c, g, 1, &r);
   return std::sqrt(r);
@@ -248,8 +254,10 @@ __global__ void __launch_bounds__(256) k_multi_axpy(long long n, const double* _
 void multi_axpy(Ctx& c, const double* Z, long long ld, int k, const double* y_host, double* x, long long n) {
   SI_CHECK(k <= 64, SEAICE_EINVAL, "multi_axpy: k > 64");
   SI_CUDA(cudaMemcpyAsync(c.scal.get() + 128, y_host, sizeof(double) * k, cudaMemcpyHostToDevice, c.s));
+  prof_begin(c);
   k_multi_axpy<<<vgrid(n), 256, 0, c.s>>>(n, Z, ld, k, c.scal.get() + 128, x);
   SI_LAUNCHED(c);
+  prof_end(c, PC_MAXPY, 8.0 * (k + 2) * n);
 }
 
 }  // namespace seaice

@@ -82,6 +82,18 @@ def struct_dict(s):
 
 
 _LIB = None
+_LIVE = __import__("weakref").WeakSet()
+
+
+def _close_all():
+    for ctx in list(_LIVE):
+        try:
+            ctx.close()
+        except Exception:
+            pass
+
+
+__import__("atexit").register(_close_all)
 
 
 def header_functions():
@@ -121,6 +133,9 @@ def lib(build_if_missing: bool = True):
             "seaice_solve_step": (C.c_int, [VP, D, D, VP, VP, VP, VP, VP, VP, P(StepStats)]),
             "seaice_solve_step_host": (C.c_int, [VP, D, D, VP, VP, VP, VP, VP, VP, P(StepStats)]),
             "seaice_launch_count": (C.c_int64, [VP]),
+            "seaice_profile_enable": (C.c_int, [VP, I32]),
+            "seaice_profile_read": (C.c_int, [VP, P(D), P(C.c_int64), P(D)]),
+            "seaice_memory": (C.c_int, [VP, P(C.c_int64), P(C.c_int64)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -187,13 +202,17 @@ class SeaIce:
         if use_torch_allocator:
             dev = self.device.index
             strm = self.stream
+            t_alloc = torch.cuda.caching_allocator_alloc
+            t_free = torch.cuda.caching_allocator_delete
 
             def _alloc(size, stream, user):
-                ptr = torch.cuda.caching_allocator_alloc(int(size), dev, strm)
-                return ptr
+                return t_alloc(int(size), dev, strm)
 
             def _free(ptr, stream, user):
-                torch.cuda.caching_allocator_delete(ptr)
+                try:
+                    t_free(ptr)
+                except Exception:  # interpreter shutdown: torch already torn down
+                    pass
 
             self._alloc_cb = ALLOC_T(_alloc)
             self._free_cb = FREE_T(_free)
@@ -205,6 +224,7 @@ class SeaIce:
         if rc != OK:
             raise SeaIceError(rc, "seaice_create failed (invalid parameters or device error)")
         self.h = h
+        _LIVE.add(self)
 
     # -- plumbing --------------------------------------------------------------
     def _check(self, rc, allow_nc=False):
@@ -235,6 +255,24 @@ class SeaIce:
     @property
     def launches(self):
         return int(self.L.seaice_launch_count(self.h))
+
+    PROF_NAMES = ["assemble", "spmv0", "cheb0", "cheb_coarse", "resid0", "multidot", "maxpy_norm", "maxpy",
+                  "delta_energy", "transfer", "coarse_solve", "resid_coarse", "pi_update"]
+
+    def profile(self, on: bool):
+        self._check(self.L.seaice_profile_enable(self.h, 1 if on else 0))
+
+    def profile_read(self):
+        ms = (C.c_double * 16)()
+        cnt = (C.c_int64 * 16)()
+        by = (C.c_double * 16)()
+        self._check(self.L.seaice_profile_read(self.h, ms, cnt, by))
+        return {name: {"ms": ms[k], "launches": cnt[k], "bytes": by[k]} for k, name in enumerate(self.PROF_NAMES)}
+
+    def memory(self):
+        live, peak = C.c_int64(), C.c_int64()
+        self.L.seaice_memory(self.h, C.byref(live), C.byref(peak))
+        return live.value, peak.value
 
     # -- API ---------------------------------------------------------------------
     def set_step(self, dt, t_new, h, A, v_prev, v_air, v_ocean, load=None):

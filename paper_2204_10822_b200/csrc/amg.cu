@@ -33,6 +33,20 @@ __host__ __device__ __forceinline__ unsigned long long salt(unsigned long long s
   return kGolden * (64ULL * seed + (unsigned long long)(level + extra));
 }
 
+// ------------------------------------------------------------------ setup phase timing (debug)
+// SEAICE_SETUP_TIMING=1 prints the wall time of each setup phase (synchronising).
+static void tick(Ctx& c, const char* what, int lvl) {
+  static const bool on = getenv("SEAICE_SETUP_TIMING") != nullptr;
+  static double last = 0.0;
+  if (!on) return;
+  cudaStreamSynchronize(c.s);
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  const double now = ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+  if (what) fprintf(stderr, "[setup] L%d %-12s %8.2f ms\n", lvl, what, now - last);
+  last = now;
+}
+
 // ------------------------------------------------------------------ scratch helpers
 struct Scratch {
   Ctx& c;
@@ -199,6 +213,24 @@ __global__ void k_bsr_spmv_dinv(int nb, const int* __restrict__ rp, const int* _
     double s = 0.0;
 #pragma unroll
     for (int b = 0; b < B; ++b) s += D[a * B + b] * acc[b];
+    y[(long long)r * B + a] = s;
+  }
+}
+
+// y_I = Dinv_I y_I (in place)
+template <int B>
+__global__ void k_dinv_apply(int nb, const double* __restrict__ dinv, double* __restrict__ y) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nb) return;
+  double v[B];
+#pragma unroll
+  for (int a = 0; a < B; ++a) v[a] = y[(long long)r * B + a];
+  const double* D = dinv + (long long)r * B * B;
+#pragma unroll
+  for (int a = 0; a < B; ++a) {
+    double s = 0.0;
+#pragma unroll
+    for (int b = 0; b < B; ++b) s += D[a * B + b] * v[b];
     y[(long long)r * B + a] = s;
   }
 }
@@ -509,6 +541,100 @@ __global__ void k_spgemm_numeric(int nr, const int* __restrict__ xrp, const int*
   }
 }
 
+// Warp-per-row variants (coarse levels have rows of hundreds of blocks): the lanes split
+// the inner loop over one Y row; an output block is touched by at most one lane per X
+// entry and the X entries are processed in order with __syncwarp between them, so each
+// output block is accumulated in exactly the same order as the thread-per-row version.
+__global__ void k_spgemm_expand_w(int nr, const int* __restrict__ xrp, const int* __restrict__ xci,
+                                  const int* __restrict__ yrp, const int* __restrict__ yci,
+                                  const long long* __restrict__ off, int* __restrict__ keys) {
+  const int r = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (r >= nr) return;
+  long long o = off[r];
+  for (int e = xrp[r]; e < xrp[r + 1]; ++e) {
+    const int j = xci[e];
+    const int f0 = yrp[j], len = yrp[j + 1] - f0;
+    for (int t = lane; t < len; t += 32) keys[o + t] = yci[f0 + t];
+    o += len;
+  }
+}
+
+__global__ void k_spgemm_count_w(int nr, const long long* __restrict__ off, const int* __restrict__ keys,
+                                 int* __restrict__ cnt) {
+  const int r = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (r > nr) return;
+  if (r == nr) {
+    if (lane == 0) cnt[r] = 0;
+    return;
+  }
+  const long long a = off[r], b = off[r + 1];
+  int u = 0;
+  for (long long base = a; base < b; base += 32) {
+    const long long k = base + lane;
+    const bool f = (k < b) && (k == a || keys[k] != keys[k - 1]);
+    u += __popc(__ballot_sync(0xffffffffu, f));
+  }
+  if (lane == 0) cnt[r] = u;
+}
+
+__global__ void k_spgemm_compact_w(int nr, const long long* __restrict__ off, const int* __restrict__ keys,
+                                   const int* __restrict__ crp, int* __restrict__ cci) {
+  const int r = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (r >= nr) return;
+  const long long a = off[r], b = off[r + 1];
+  int o = crp[r];
+  for (long long base = a; base < b; base += 32) {
+    const long long k = base + lane;
+    const bool f = (k < b) && (k == a || keys[k] != keys[k - 1]);
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    if (f) cci[o + __popc(m & ((1u << lane) - 1u))] = keys[k];
+    o += __popc(m);
+  }
+}
+
+template <int M, int K, int P>
+__global__ void k_spgemm_numeric_w(int nr, const int* __restrict__ xrp, const int* __restrict__ xci,
+                                   const double* __restrict__ xv, const int* __restrict__ yrp,
+                                   const int* __restrict__ yci, const double* __restrict__ yv,
+                                   const int* __restrict__ crp, const int* __restrict__ cci, double* __restrict__ cv) {
+  const int r = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (r >= nr) return;
+  const int c0 = crp[r], c1 = crp[r + 1];
+  for (long long t = (long long)c0 * M * P + lane; t < (long long)c1 * M * P; t += 32) cv[t] = 0.0;
+  __syncwarp();
+  for (int e = xrp[r]; e < xrp[r + 1]; ++e) {
+    const int j = xci[e];
+    double xb[M * K];
+#pragma unroll
+    for (int t = 0; t < M * K; ++t) xb[t] = xv[(long long)e * M * K + t];
+    int lo_hint = c0;
+    for (int f = yrp[j] + lane; f < yrp[j + 1]; f += 32) {
+      const int col = yci[f];
+      int lo = lo_hint, hi = c1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cci[mid] < col) lo = mid + 1;
+        else hi = mid;
+      }
+      lo_hint = lo;
+      double* cb = cv + (long long)lo * M * P;
+      const double* yb = yv + (long long)f * K * P;
+#pragma unroll
+      for (int a = 0; a < M; ++a)
+#pragma unroll
+        for (int b = 0; b < P; ++b) {
+          double s = cb[a * P + b];
+#pragma unroll
+          for (int k = 0; k < K; ++k) s += xb[a * K + k] * yb[k * P + b];
+          cb[a * P + b] = s;
+        }
+    }
+    __syncwarp();
+  }
+}
+
+static int wgrid(long long rows) { return (int)((rows * 32 + 255) / 256); }
+
 struct BsrMat {
   int nbr = 0, nbc = 0, br = 0, bc = 0;
   long long nnzb = 0;
@@ -531,7 +657,11 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
   const long long total = read_scalar(c, off + nr);
   int* k1 = S.get<int>(total);
   int* k2 = S.get<int>(total);
-  k_spgemm_expand<<<grid_for(nr), kThreads, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, off, k1);
+  const bool wide = total > 48LL * nr;  // long rows: warp per row
+  if (wide)
+    k_spgemm_expand_w<<<wgrid(nr), 256, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, off, k1);
+  else
+    k_spgemm_expand<<<grid_for(nr), kThreads, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, off, k1);
   SI_LAUNCHED(c);
   {
     cub::DoubleBuffer<int> db(k1, k2);
@@ -544,7 +674,10 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
     k1 = db.Current();
   }
   int* cnt = S.get<int>(nr + 1);
-  k_spgemm_count<<<grid_for(nr + 1), kThreads, 0, c.s>>>(nr, off, k1, cnt);
+  if (wide)
+    k_spgemm_count_w<<<wgrid(nr + 1), 256, 0, c.s>>>(nr, off, k1, cnt);
+  else
+    k_spgemm_count<<<grid_for(nr + 1), kThreads, 0, c.s>>>(nr, off, k1, cnt);
   SI_LAUNCHED(c);
   crp.ensure(c.al, nr + 1);
   exclusive_scan(c, cnt, crp.get(), nr + 1);
@@ -552,10 +685,17 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
   SI_CHECK(cnnzb < (1LL << 31), SEAICE_EINVAL, "SpGEMM result exceeds int32 indexing");
   cci.ensure(c.al, cnnzb);
   cval.ensure(c.al, cnnzb * M * P);
-  k_spgemm_compact<<<grid_for(nr), kThreads, 0, c.s>>>(nr, off, k1, crp.get(), cci.get());
-  SI_LAUNCHED(c);
-  k_spgemm_numeric<M, K, P><<<grid_for(nr, 128), 128, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp.get(),
-                                                                 cci.get(), cval.get());
+  if (wide) {
+    k_spgemm_compact_w<<<wgrid(nr), 256, 0, c.s>>>(nr, off, k1, crp.get(), cci.get());
+    SI_LAUNCHED(c);
+    k_spgemm_numeric_w<M, K, P><<<wgrid(nr), 256, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp.get(),
+                                                            cci.get(), cval.get());
+  } else {
+    k_spgemm_compact<<<grid_for(nr), kThreads, 0, c.s>>>(nr, off, k1, crp.get(), cci.get());
+    SI_LAUNCHED(c);
+    k_spgemm_numeric<M, K, P><<<grid_for(nr, 128), 128, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val,
+                                                                   crp.get(), cci.get(), cval.get());
+  }
   SI_LAUNCHED(c);
 }
 
@@ -887,6 +1027,157 @@ __global__ void k_bsr_spmv_add(int nb, const int* __restrict__ rp, const int* __
   for (int a = 0; a < BR; ++a) y[(long long)r * BR + a] = acc[a];
 }
 
+// ------------------------------------------------------------------ group-per-row BSR kernels
+// G consecutive lanes own one block row: lane l reads blocks e = rp[row] + l, + G, ...
+// so the G blocks a group touches per step are contiguous in memory (coalesced), and the
+// BR partial sums are combined with an xor-butterfly (same order on every lane).
+template <int BR, int BC, int G>
+__device__ __forceinline__ void grp_row(int row, int nb, int lig, const int* __restrict__ rp,
+                                        const int* __restrict__ ci, const double* __restrict__ val,
+                                        const double* __restrict__ x, double acc[BR]) {
+#pragma unroll
+  for (int a = 0; a < BR; ++a) acc[a] = 0.0;
+  if (row < nb) {
+    const int e1 = __ldg(rp + row + 1);
+    for (int e = __ldg(rp + row) + lig; e < e1; e += G) {
+      const int col = __ldg(ci + e);
+      double xv[BC];
+#pragma unroll
+      for (int b = 0; b < BC; ++b) xv[b] = __ldg(x + (long long)col * BC + b);
+      const double* v = val + (long long)e * BR * BC;
+#pragma unroll
+      for (int a = 0; a < BR; ++a)
+#pragma unroll
+        for (int b = 0; b < BC; ++b) acc[a] += __ldg(v + a * BC + b) * xv[b];
+    }
+  }
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1)
+#pragma unroll
+    for (int a = 0; a < BR; ++a) acc[a] += __shfl_xor_sync(0xffffffffu, acc[a], off, G);
+}
+
+// y = A x (add = 0) or y += A x (add = 1)
+template <int BR, int BC, int G>
+__global__ void __launch_bounds__(256) k_gspmv(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                                               const double* __restrict__ val, const double* __restrict__ x,
+                                               double* __restrict__ y, int add) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int row = (int)(t / G), lig = (int)(t % G);
+  double acc[BR];
+  grp_row<BR, BC, G>(row, nb, lig, rp, ci, val, x, acc);
+  if (row < nb && lig == 0) {
+#pragma unroll
+    for (int a = 0; a < BR; ++a) {
+      const long long i = (long long)row * BR + a;
+      y[i] = add ? y[i] + acc[a] : acc[a];
+    }
+  }
+}
+
+// fused Chebyshev step (same semantics as k_cheb_stencil) on a coarse level
+template <int B, int G>
+__global__ void __launch_bounds__(256) k_gcheb(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                                               const double* __restrict__ val, const double* __restrict__ dinv,
+                                               const double* __restrict__ d, double* __restrict__ r,
+                                               double* __restrict__ x, double* __restrict__ dout, double c1,
+                                               double c2, int first, int want_r, int want_d) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int row = (int)(t / G), lig = (int)(t % G);
+  double acc[B];
+  if (want_r) grp_row<B, B, G>(row, nb, lig, rp, ci, val, d, acc);
+  if (row >= nb || lig != 0) return;
+  double dv[B];
+#pragma unroll
+  for (int a = 0; a < B; ++a) {
+    const long long i = (long long)row * B + a;
+    dv[a] = d[i];
+    x[i] = (first ? 0.0 : x[i]) + dv[a];
+  }
+  if (!want_r) return;
+  double rv[B];
+#pragma unroll
+  for (int a = 0; a < B; ++a) {
+    const long long i = (long long)row * B + a;
+    rv[a] = r[i] - acc[a];
+    r[i] = rv[a];
+  }
+  if (want_d) {
+    const double* D = dinv + (long long)row * B * B;
+#pragma unroll
+    for (int a = 0; a < B; ++a) {
+      double z = 0.0;
+#pragma unroll
+      for (int b = 0; b < B; ++b) z += D[a * B + b] * rv[b];
+      dout[(long long)row * B + a] = c1 * dv[a] + c2 * z;
+    }
+  }
+}
+
+// r = b - A x (x may be NULL: r = b); d = c2 Dinv r
+template <int B, int G>
+__global__ void __launch_bounds__(256) k_gresid(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                const double* __restrict__ val, const double* __restrict__ dinv,
+                                                const double* __restrict__ b, const double* __restrict__ x,
+                                                double* __restrict__ r, double* __restrict__ d, double c2) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int row = (int)(t / G), lig = (int)(t % G);
+  double acc[B];
+  if (x) grp_row<B, B, G>(row, nb, lig, rp, ci, val, x, acc);
+  else {
+#pragma unroll
+    for (int a = 0; a < B; ++a) acc[a] = 0.0;
+  }
+  if (row >= nb || lig != 0) return;
+  double rv[B];
+#pragma unroll
+  for (int a = 0; a < B; ++a) {
+    const long long i = (long long)row * B + a;
+    rv[a] = b[i] - acc[a];
+    r[i] = rv[a];
+  }
+  const double* D = dinv + (long long)row * B * B;
+#pragma unroll
+  for (int a = 0; a < B; ++a) {
+    double z = 0.0;
+#pragma unroll
+    for (int bb = 0; bb < B; ++bb) z += D[a * B + bb] * rv[bb];
+    d[(long long)row * B + a] = c2 * z;
+  }
+}
+
+static int pick_group(long long nnzb, int nb) {
+  const double avg = nb > 0 ? (double)nnzb / nb : 1.0;
+  if (avg <= 6.0) return 4;
+  if (avg <= 14.0) return 8;
+  if (avg <= 40.0) return 16;
+  return 32;
+}
+static int ggrid(int nb, int G) { return (int)(((long long)nb * G + 255) / 256); }
+
+#define SI_GDISPATCH(G, CALL) \
+  switch (G) {                \
+    case 4: { constexpr int GG = 4; CALL; } break;   \
+    case 8: { constexpr int GG = 8; CALL; } break;   \
+    case 16: { constexpr int GG = 16; CALL; } break; \
+    default: { constexpr int GG = 32; CALL; } break; \
+  }
+
+static void gspmv(Ctx& c, int nb, int br, int bc, long long nnzb, const int* rp, const int* ci, const double* val,
+                  const double* x, double* y, int add) {
+  const int G = pick_group(nnzb, nb);
+  if (br == 3 && bc == 3) {
+    SI_GDISPATCH(G, (k_gspmv<3, 3, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, y, add)))
+  } else if (br == 2 && bc == 3) {
+    SI_GDISPATCH(G, (k_gspmv<2, 3, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, y, add)))
+  } else if (br == 3 && bc == 2) {
+    SI_GDISPATCH(G, (k_gspmv<3, 2, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, y, add)))
+  } else {
+    SI_GDISPATCH(G, (k_gspmv<2, 2, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, y, add)))
+  }
+  SI_LAUNCHED(c);
+}
+
 // ------------------------------------------------------------------ host: setup
 static BsrMat view(Level& L) { return BsrMat{L.nb, L.nb, L.b, L.b, L.nnzb, L.rp.get(), L.ci.get(), L.val.get()}; }
 
@@ -903,8 +1194,8 @@ static double power_lambda(Ctx& c, Level& L, int lvl) {
   nx = 1.0;
   double lam = 0.0;
   for (int it = 0; it < c.p.power_iters; ++it) {
-    k_bsr_spmv_dinv<B><<<grid_for(L.nb), kThreads, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.val.get(),
-                                                             L.dinv.get(), x, y);
+    gspmv(c, L.nb, B, B, L.nnzb, L.rp.get(), L.ci.get(), L.val.get(), x, y, 0);
+    k_dinv_apply<B><<<grid_for(L.nb), kThreads, 0, c.s>>>(L.nb, L.dinv.get(), y);
     SI_LAUNCHED(c);
     const double ny = norm2(c, y, N);
     lam = ny / nx;
@@ -1015,12 +1306,14 @@ static void build_transfer(Ctx& c, Level& L, Level& Lc, int lvl, int na, Scratch
   Lc.B.ensure(c.al, (size_t)na * 9);
   k_tentative<B><<<grid_for(na, 128), 128, 0, c.s>>>(na, start, members, L.B.get(), ptrp, ptval, Lc.B.get());
   SI_LAUNCHED(c);
+  tick(c, "tentative", lvl);
   BsrMat Pt{nb, na, B, 3, ptn, ptrp, ptci, ptval};
   // T = A P_tent ; P = P_tent - omega Dinv T  (pattern of T)
   DBuf<int> trp, tci;
   DBuf<double> tval;
   long long tn = 0;
   spgemm<B, B, 3>(c, view(L), Pt, trp, tci, tval, tn);
+  tick(c, "A*Pt", lvl);
   L.Prp.free_();
   L.Pci.free_();
   L.Pval.free_();
@@ -1035,17 +1328,21 @@ static void build_transfer(Ctx& c, Level& L, Level& Lc, int lvl, int na, Scratch
   tval.free_();
   L.nbc = na;
   BsrMat P{nb, na, B, 3, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.Pval.get()};
+  tick(c, "smoothP", lvl);
   // R = P^T
   transpose<B, 3>(c, P, L.Rrp, L.Rci, L.Rval);
   L.Rnnzb = L.Pnnzb;
+  tick(c, "transpose", lvl);
   // A_c = R (A P)
   DBuf<int> aprp, apci;
   DBuf<double> apval;
   long long apn = 0;
   spgemm<B, B, 3>(c, view(L), P, aprp, apci, apval, apn);
+  tick(c, "A*P", lvl);
   BsrMat AP{nb, na, B, 3, apn, aprp.get(), apci.get(), apval.get()};
   BsrMat R{na, nb, 3, B, L.Rnnzb, L.Rrp.get(), L.Rci.get(), L.Rval.get()};
   spgemm<3, B, 3>(c, R, AP, Lc.rp, Lc.ci, Lc.val, Lc.nnzb);
+  tick(c, "R*AP", lvl);
   aprp.free_();
   apci.free_();
   apval.free_();
@@ -1126,9 +1423,12 @@ void amg_setup_impl(Ctx& c) {
     Level& L = c.lv[lvl];
     Scratch S(c);
     double* dnorm = S.get<double>(L.nb);
+    tick(c, nullptr, lvl);
     if (L.b == 2) level_diag<2>(c, L, S, dnorm);
     else level_diag<3>(c, L, S, dnorm);
+    tick(c, "diag", lvl);
     L.lmax = (L.b == 2) ? power_lambda<2>(c, L, lvl) : power_lambda<3>(c, L, lvl);
+    tick(c, "power", lvl);
     nnz_total += L.nnzb * L.b * L.b;
     const long long ndof = (long long)L.nb * L.b;
     // work vectors for the V-cycle
@@ -1136,6 +1436,7 @@ void amg_setup_impl(Ctx& c) {
     const bool last_allowed = (lvl + 1 >= c.p.max_levels);
     if (ndof <= c.p.coarse_max_dof || last_allowed) break;
     const int na = (L.b == 2) ? aggregate_level<2>(c, L, lvl, dnorm, S) : aggregate_level<3>(c, L, lvl, dnorm, S);
+    tick(c, "aggregate", lvl);
     if (na == 0 || na > 0.9 * L.nb) break;
     c.lv.emplace_back();
     Level& Lc = c.lv.back();
@@ -1146,7 +1447,9 @@ void amg_setup_impl(Ctx& c) {
   Level& Lc = c.lv.back();
   const long long nd = (long long)Lc.nb * Lc.b;
   SI_CHECK(nd <= 8192, SEAICE_EINVAL, "AMG coarsest level too large for the dense solve (coarsening stalled)");
+  tick(c, nullptr, (int)c.lv.size() - 1);
   coarse_factor(c, Lc);
+  tick(c, "coarse", (int)c.lv.size() - 1);
   const int flag = read_scalar(c, c.flag.get());
   SI_CHECK(!(flag & 4), SEAICE_ENONFINITE, "AMG: singular diagonal block");
   SI_CHECK(!(flag & 8), SEAICE_ENONFINITE, "AMG: coarse matrix not positive definite");
@@ -1183,12 +1486,11 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
     k_resid_dinv_stencil<<<grid_for(c.Nn), 256, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L.dinv.get(),
                                                           (const double2*)b, pre ? nullptr : (const double2*)x,
                                                           (double2*)r, (double2*)d, 1.0 / k.th);
-  } else if (L.b == 3) {
-    k_resid_dinv_bsr<3><<<grid_for(L.nb), kThreads, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.val.get(),
-                                                               L.dinv.get(), b, pre ? nullptr : x, r, d, 1.0 / k.th);
   } else {
-    k_resid_dinv_bsr<2><<<grid_for(L.nb), kThreads, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.val.get(),
-                                                               L.dinv.get(), b, pre ? nullptr : x, r, d, 1.0 / k.th);
+    const int G = pick_group(L.nnzb, L.nb);
+    SI_GDISPATCH(G, (k_gresid<3, GG><<<ggrid(L.nb, GG), 256, 0, c.s>>>(
+                        L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), b, pre ? nullptr : x, r, d,
+                        1.0 / k.th)))
   }
   SI_LAUNCHED(c);
   {
@@ -1209,12 +1511,11 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
       k_cheb_stencil<<<grid_for(c.Nn), 256, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L.dinv.get(), (const double2*)d,
                                                      (double2*)r, (double2*)x, (double2*)d2, c1, c2, first, want_r,
                                                      want_d);
-    } else if (L.b == 3) {
-      k_cheb_bsr<3><<<grid_for(L.nb), kThreads, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), d,
-                                                           r, x, d2, c1, c2, first, want_r, want_d);
     } else {
-      k_cheb_bsr<2><<<grid_for(L.nb), kThreads, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), d,
-                                                           r, x, d2, c1, c2, first, want_r, want_d);
+      const int G = pick_group(L.nnzb, L.nb);
+      SI_GDISPATCH(G, (k_gcheb<3, GG><<<ggrid(L.nb, GG), 256, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.val.get(),
+                                                                       L.dinv.get(), d, r, x, d2, c1, c2, first,
+                                                                       want_r, want_d)))
     }
     SI_LAUNCHED(c);
     {
@@ -1242,18 +1543,12 @@ static void vcycle_level(Ctx& c, int l, const double* b, double* x) {
   Level& Lc = c.lv[l + 1];
   // r_c = R r
   prof_begin(c);
-  bsr_apply(c, L.nbc, 3, L.b, L.Rrp.get(), L.Rci.get(), L.Rval.get(), L.r.get(), Lc.rhs.get());
+  gspmv(c, L.nbc, 3, L.b, L.Rnnzb, L.Rrp.get(), L.Rci.get(), L.Rval.get(), L.r.get(), Lc.rhs.get(), 0);
   prof_end(c, PC_TRANSFER, L.Rnnzb * (24.0 * L.b + 4.0) + 4.0 * (L.nbc + 1) + 8.0 * L.b * L.nb + 24.0 * L.nbc);
   vcycle_level(c, l + 1, Lc.rhs.get(), Lc.x.get());
   // x += P e_c
   prof_begin(c);
-  if (L.b == 2)
-    k_bsr_spmv_add<2, 3><<<grid_for(L.nb), kThreads, 0, c.s>>>(L.nb, L.Prp.get(), L.Pci.get(), L.Pval.get(),
-                                                               Lc.x.get(), x);
-  else
-    k_bsr_spmv_add<3, 3><<<grid_for(L.nb), kThreads, 0, c.s>>>(L.nb, L.Prp.get(), L.Pci.get(), L.Pval.get(),
-                                                               Lc.x.get(), x);
-  SI_LAUNCHED(c);
+  gspmv(c, L.nb, L.b, 3, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.Pval.get(), Lc.x.get(), x, 1);
   prof_end(c, PC_TRANSFER, L.Pnnzb * (24.0 * L.b + 4.0) + 4.0 * (L.nb + 1) + 16.0 * L.b * L.nb + 24.0 * L.nbc);
   smooth(c, l, b, x, false);
 }

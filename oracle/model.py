@@ -298,9 +298,11 @@ class Problem:
             phi -= float(self.load @ v)
         return phi
 
-    def delta_energy(self, v, vt, alpha):
+    def delta_energy(self, v, vt, alpha, with_abs=False):
         """Phi(v + alpha vt) - Phi(v) in difference form (reading G12):
-        the Delta and |w|^3 differences are rewritten so no O(Phi) terms cancel."""
+        the Delta and |w|^3 differences are rewritten so no O(Phi) terms cancel.
+        with_abs=True also returns S = sum_q w (|t_mass| + dt(|t_plast| + |t_ocean| + |t_lin|))
+        (+ |alpha load.vt|), the scale of the roundoff in the sum (reading G12b)."""
         prm, dt = self.prm, self.dt
         cells = self.cells_all()
         val0, eps0, tau0, D0 = self.kinematics(v, cells)
@@ -313,7 +315,10 @@ class Problem:
         P = self.P[:, None]
         rh = self.rhoh[:, None]
         a = alpha
-        t_mass = 0.5 * rh * a * np.sum(dv * (2.0 * val0 + a * dv), -1) - rh * a * np.sum(vn * dv, -1)
+        # 1/2 rho h (|v+a vt|^2 - |v|^2) - rho h v^n.(a vt) = rho h a vt.(v - v^n) + 1/2 rho h a^2 |vt|^2,
+        # with v - v^n interpolated from NODAL differences (no cancellation when v ~ v^n)
+        dvn, _ = self.at_qp(v - self.v_prev, cells)
+        t_mass = rh * a * np.sum(dv * dvn, -1) + 0.5 * rh * a * a * np.sum(dv * dv, -1)
         dDelta = 2.0 * a * frob(dtau, 2.0 * tau0 + a * dtau) / (D1 + D0)
         t_plast = 0.5 * P * (dDelta - a * trace(deps))
         w0 = vo - val0
@@ -321,14 +326,19 @@ class Problem:
         n0 = np.linalg.norm(w0, axis=-1)
         n1 = np.linalg.norm(w1, axis=-1)
         den = n1 + n0
-        dn = np.where(den > 0, np.sum((w1 - w0) * (w1 + w0), -1) / np.where(den > 0, den, 1.0), 0.0)
+        # |w1| - |w0| = (w1 - w0).(w1 + w0)/(|w1| + |w0|) with w1 - w0 = -a vt taken exactly
+        # (forming w1 - w0 from w1 would lose |w0|/|a vt| digits)
+        dn = np.where(den > 0, np.sum((-a * dv) * (2.0 * w0 - a * dv), -1) / np.where(den > 0, den, 1.0), 0.0)
         t_ocean = prm.C_o * prm.rho_o / 3.0 * dn * (n1 * n1 + n1 * n0 + n0 * n0)
         t_lin = a * rh * prm.f_c * np.sum(e_r_cross(vn - vo) * dv, -1) - a * np.sum(tau_atm(va, prm) * dv, -1)
         integrand = t_mass + dt * (t_plast + t_ocean + t_lin)
         d = float(np.sum(integrand * self.w[None, :]))
+        S = float(np.sum((np.abs(t_mass) + dt * (np.abs(t_plast) + np.abs(t_ocean) + np.abs(t_lin))) * self.w[None, :]))
         if self.load is not None:
-            d -= float(a * (self.load @ vt))
-        return d
+            lv = float(a * (self.load @ vt))
+            d -= lv
+            S += abs(lv)
+        return (d, S) if with_abs else d
 
     # -- dual variable --------------------------------------------------------
     @staticmethod

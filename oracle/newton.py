@@ -15,6 +15,11 @@ import numpy as np
 from . import krylov
 from .model import Problem
 
+# Reading G12b: |DeltaPhi| <= LS_ETA * S (S = sum of |terms|) is indistinguishable from 0 in
+# fp64; such a step is accepted iff it reduces ||R||_2 (the paper's residual-based
+# backtracking, "results in similar results").
+LS_ETA = 1e-12
+
 
 def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
                ls_max=20, krylov_rtol=1e-8, krylov_maxit=300, restart=30,
@@ -65,8 +70,13 @@ def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
         alpha, dphi, stag, halv = 1.0, 0.0, True, 0
         for k in range(ls_max + 1):
             alpha = 0.5 ** k
-            dphi = pb.delta_energy(v, vt, alpha)
-            if dphi < 0.0:
+            dphi, S = pb.delta_energy(v, vt, alpha, with_abs=True)
+            if dphi < -LS_ETA * S:
+                stag = False
+                halv = k
+                break
+            if dphi <= LS_ETA * S and np.linalg.norm(pb.residual(v + alpha * vt)) < nr:
+                # energy change below roundoff: residual-based acceptance (reading G12b)
                 stag = False
                 halv = k
                 break

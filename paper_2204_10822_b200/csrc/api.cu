@@ -30,6 +30,9 @@ struct seaice_ctx {
 
 namespace {
 
+// Reading G12b: |DeltaPhi| <= kLsEta * sum|terms| is fp64 roundoff.
+constexpr double kLsEta = 1e-12;
+
 struct EvTimer {
   Ctx& c;
   explicit EvTimer(Ctx& cc) : c(cc) { SI_CUDA(cudaEventRecord(c.ev0, c.s)); }
@@ -105,17 +108,31 @@ int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* o
   {
     EvTimer t(c);
     const int K = c.p.ls_max_halvings + 1;
-    std::vector<double> al(K), dphi(K);
+    std::vector<double> al(K), dphi(K), sab(K);
     for (int k = 0; k < K; ++k) al[k] = std::ldexp(1.0, -k);
     int acc = -1;
+    const double nr0 = st.res_norm;
     for (int k0 = 0; k0 < K && acc < 0; k0 += 8) {
       const int cnt = std::min(8, K - k0);
-      delta_energy_impl(c, v, c.vt.get(), al.data() + k0, cnt, dphi.data() + k0);
-      for (int k = k0; k < k0 + cnt; ++k)
-        if (dphi[k] < 0.0) {
+      delta_energy_impl(c, v, c.vt.get(), al.data() + k0, cnt, dphi.data() + k0, sab.data() + k0);
+      for (int k = k0; k < k0 + cnt; ++k) {
+        if (dphi[k] < -kLsEta * sab[k]) {
           acc = k;
           break;
         }
+        if (dphi[k] <= kLsEta * sab[k]) {
+          // energy change below fp64 roundoff: accept iff ||R|| decreases (reading G12b)
+          c.w.ensure(c.al, c.N);
+          copy(c, c.w.get(), v, c.N);
+          axpy(c, al[k], c.vt.get(), c.w.get(), c.N);
+          double nr1 = 0.0;
+          assemble_impl(c, c.w.get(), nullptr, false, nullptr, &nr1);
+          if (nr1 < nr0) {
+            acc = k;
+            break;
+          }
+        }
+      }
     }
     if (acc < 0) {
       st.ls_stagnated = 1;
@@ -199,7 +216,7 @@ void seaice_default_params(seaice_params* p, int32_t n) {
   p->cheb_degree = 3;
   p->coarse_max_dof = 1200;
   p->max_levels = 25;
-  p->cheb_lower = 0.1;
+  p->cheb_lower = 0.03;
   p->cheb_upper = 1.1;
   p->power_iters = 20;
   p->project_pi = 0;

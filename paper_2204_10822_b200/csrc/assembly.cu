@@ -296,11 +296,12 @@ __global__ void __launch_bounds__(128) k_delta_energy(Phys ph, int Nc, const dou
                                                       const double* __restrict__ alphas_d, int count,
                                                       double* __restrict__ part) {
   __shared__ double sh[32];
-  double acc[kMaxAlpha];
+  double acc[kMaxAlpha], sab[kMaxAlpha];
   double al[kMaxAlpha];
 #pragma unroll
   for (int k = 0; k < kMaxAlpha; ++k) {
     acc[k] = 0.0;
+    sab[k] = 0.0;
     al[k] = (k < count) ? alphas_d[k] : 0.0;
   }
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(128) k_delta_energy(Phys ph, int Nc, const dou
     const double dmin2 = ph.delta_min * ph.delta_min;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      double x0 = 0, y0 = 0, xt = 0, yt = 0, xn = 0, yn = 0, xo = 0, yo = 0, xa = 0, ya = 0;
+      double x0 = 0, y0 = 0, xt = 0, yt = 0, xn = 0, yn = 0, xo = 0, yo = 0, xa = 0, ya = 0, xd = 0, yd = 0;
       double A00 = 0, A01 = 0, A10 = 0, A11 = 0, B00 = 0, B01 = 0, B10 = 0, B11 = 0;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
@@ -327,6 +328,7 @@ __global__ void __launch_bounds__(128) k_delta_energy(Phys ph, int Nc, const dou
         x0 += N * u[b][0]; y0 += N * u[b][1];
         xt += N * ut[b][0]; yt += N * ut[b][1];
         xn += N * un[b][0]; yn += N * un[b][1];
+        xd += N * (u[b][0] - un[b][0]); yd += N * (u[b][1] - un[b][1]);  // v - v^n from nodal differences
         xo += N * uo[b][0]; yo += N * uo[b][1];
         xa += N * ua[b][0]; ya += N * ua[b][1];
         A00 += u[b][0] * Gx(q, b); A01 += u[b][0] * Gy(q, b); A10 += u[b][1] * Gx(q, b); A11 += u[b][1] * Gy(q, b);
@@ -342,13 +344,15 @@ __global__ void __launch_bounds__(128) k_delta_energy(Phys ph, int Nc, const dou
       // linear terms: rho h f_c (e_r x (v^n - v_o)).vt - tau_atm.vt
       const double dux = xn - xo, duy = yn - yo;
       const double lin = rh * ph.f_c * (-duy * xt + dux * yt) - sa * (xa * xt + ya * yt);
-      const double vtv0 = xt * x0 + yt * y0, vtvt = xt * xt + yt * yt, vnvt = xn * xt + yn * yt;
+      const double vtd = xt * xd + yt * yd, vtvt = xt * xt + yt * yt;
       const double tt_t0 = dot3(tt, t0), tt_tt = dot3(tt, tt);
+      const double vt_w0 = xt * w0x + yt * w0y;
 #pragma unroll
       for (int k = 0; k < kMaxAlpha; ++k) {
         if (k < count) {
           const double a = al[k];
-          const double tmass = 0.5 * rh * a * (2.0 * vtv0 + a * vtvt) - rh * a * vnvt;
+          // 1/2 rho h (|v + a vt|^2 - |v|^2) - rho h v^n.(a vt) = rho h a vt.(v - v^n) + 1/2 rho h a^2 |vt|^2
+          const double tmass = rh * a * vtd + 0.5 * rh * a * a * vtvt;
           const V3 t1{t0.x + a * tt.x, t0.y + a * tt.y, t0.z + a * tt.z};
           const double D1 = sqrt(dmin2 + 2.0 * dot3(t1, t1));
           const double dD = 2.0 * a * (2.0 * tt_t0 + a * tt_tt) / (D1 + D0);
@@ -356,9 +360,11 @@ __global__ void __launch_bounds__(128) k_delta_energy(Phys ph, int Nc, const dou
           const double w1x = w0x - a * xt, w1y = w0y - a * yt;
           const double n1 = sqrt(w1x * w1x + w1y * w1y);
           const double den = n1 + n0;
-          const double dn = den > 0.0 ? ((w1x - w0x) * (w1x + w0x) + (w1y - w0y) * (w1y + w0y)) / den : 0.0;
+          // |w1| - |w0| = (w1 - w0).(w1 + w0)/(|w1| + |w0|), w1 - w0 = -a vt taken exactly
+          const double dn = den > 0.0 ? (-a) * (2.0 * vt_w0 - a * vtvt) / den : 0.0;
           const double toc = co3 * dn * (n1 * n1 + n1 * n0 + n0 * n0);
           acc[k] += w * (tmass + dt * (tpl + toc + a * lin));
+          sab[k] += w * (fabs(tmass) + dt * (fabs(tpl) + fabs(toc) + fabs(a * lin)));
         }
       }
     }
@@ -366,8 +372,10 @@ __global__ void __launch_bounds__(128) k_delta_energy(Phys ph, int Nc, const dou
 #pragma unroll
   for (int k = 0; k < kMaxAlpha; ++k) {
     if (k < count) {
-      double bs = block_sum(acc[k], sh);
+      const double bs = block_sum(acc[k], sh);
       if (threadIdx.x == 0) part[(long long)k * gridDim.x + blockIdx.x] = bs;
+      const double bsa = block_sum(sab[k], sh);
+      if (threadIdx.x == 0) part[(long long)(kMaxAlpha + k) * gridDim.x + blockIdx.x] = bsa;
     }
   }
 }
@@ -546,11 +554,12 @@ static double finish_sum(Ctx& c, const double* part, int nparts) {
   return c.hbuf[0];
 }
 
-void delta_energy_impl(Ctx& c, const double* v, const double* vt, const double* alphas, int count, double* out) {
+void delta_energy_impl(Ctx& c, const double* v, const double* vt, const double* alphas, int count, double* out,
+                       double* sabs) {
   SI_CHECK(c.step_set, SEAICE_ESTATE, "delta_energy before set_step");
   SI_CHECK(count >= 1 && count <= 32, SEAICE_EINVAL, "delta_energy: 1 <= count <= 32");
   const int g = grid_for(c.Nc, 128);
-  c.part.ensure(c.al, (size_t)g * kMaxAlpha + 64);
+  c.part.ensure(c.al, (size_t)g * 2 * kMaxAlpha + 64);
   for (int k0 = 0; k0 < count; k0 += kMaxAlpha) {
     const int cnt = std::min(kMaxAlpha, count - k0);
     std::memcpy(c.hbuf, alphas + k0, sizeof(double) * cnt);
@@ -560,15 +569,21 @@ void delta_energy_impl(Ctx& c, const double* v, const double* vt, const double* 
                                         c.rhoh.get(), c.scal.get() + 32, cnt, c.part.get());
     SI_LAUNCHED(c);
     prof_end(c, PC_DENERGY, 80.0 * c.Nn + 16.0 * c.Nc);
-    k_sum_partials<<<1, 1024, 0, c.s>>>(c.part.get(), g, cnt, g, c.scal.get());
+    k_sum_partials<<<1, 1024, 0, c.s>>>(c.part.get(), g, 2 * kMaxAlpha, g, c.scal.get());
     SI_LAUNCHED(c);
-    SI_CUDA(cudaMemcpyAsync(c.hbuf, c.scal.get(), sizeof(double) * cnt, cudaMemcpyDeviceToHost, c.s));
+    SI_CUDA(cudaMemcpyAsync(c.hbuf, c.scal.get(), sizeof(double) * 2 * kMaxAlpha, cudaMemcpyDeviceToHost, c.s));
     SI_CUDA(cudaStreamSynchronize(c.s));
-    for (int k = 0; k < cnt; ++k) out[k0 + k] = c.hbuf[k];
+    for (int k = 0; k < cnt; ++k) {
+      out[k0 + k] = c.hbuf[k];
+      if (sabs) sabs[k0 + k] = c.hbuf[kMaxAlpha + k];
+    }
   }
   if (c.have_load) {
     const double lv = dot(c, c.load.get(), vt, c.N);
-    for (int k = 0; k < count; ++k) out[k] -= alphas[k] * lv;
+    for (int k = 0; k < count; ++k) {
+      out[k] -= alphas[k] * lv;
+      if (sabs) sabs[k] += std::fabs(alphas[k] * lv);
+    }
   }
 }
 

@@ -176,7 +176,8 @@ void set_step_impl(Ctx& c, double dt, double t_new, const double* h, const doubl
                    const double* v_air, const double* v_ocean, const double* load);
 void assemble_impl(Ctx& c, const double* v, const double* pi, bool jacobian, double* r_out, double* norm_host);
 void build_csr_view(Ctx& c, seaice_csr* out);
-void delta_energy_impl(Ctx& c, const double* v, const double* vt, const double* alphas, int count, double* out);
+void delta_energy_impl(Ctx& c, const double* v, const double* vt, const double* alphas, int count, double* out,
+                       double* sabs = nullptr);
 void pi_tilde_impl(Ctx& c, const double* v, const double* pi, const double* vt, double* out, double alpha,
                    bool update_in_place);
 

@@ -146,6 +146,26 @@ def test_amg_fgmres_counts_parity(n, it):
     assert np.linalg.norm(np_(xg) - xd) <= 1e-6 * np.linalg.norm(xd)
 
 
+def test_multistep_parity_moving_cyclone():
+    """Three consecutive implicit steps with the moving cyclone (warm starts, where the energy
+    line search must resolve tiny decreases, reading G12/G12b): Newton counts +-1 and v to
+    1e-8 per step vs the oracle with direct solves."""
+    n = 64
+    cfg = wl.Config("ms64", n, 1, 3, True)
+    hA = wl.ice_fields(cfg)
+    ctx = make_ctx(n, krylov_rtol=1e-10)
+    vo_ = None
+    vg = torch.zeros(ctx.N, dtype=torch.float64, device="cuda")
+    for s in range(3):
+        inp = wl.step_inputs(cfg, s, v_prev=vo_, h_A=hA)
+        vo_, _, ho = newton.solve_step(inp, PRM)
+        vin = vg.clone()
+        vg, st = ctx.solve_step(inp.dt, inp.t_new, inp.h, inp.A, vin, inp.v_air, inp.v_ocean)
+        assert st["converged"] == 1, (s, st)
+        assert abs(st["newton_iters"] - ho["newton_iters"]) <= 1, (s, st["newton_iters"], ho["newton_iters"])
+        assert np.linalg.norm(np_(vg) - vo_) <= 1e-8 * np.linalg.norm(vo_), s
+
+
 def test_newton_amg_config1_parity():
     """Config 1 implicit step with the product path (AMG-FGMRES): Newton count +-1 and
     converged v to 1e-8 relative L2 vs the oracle with direct solves."""

@@ -48,29 +48,26 @@ static void tick(Ctx& c, const char* what, int lvl) {
 }
 
 // ------------------------------------------------------------------ scratch helpers
+// Setup scratch from the context arena; released (LIFO) when the Scratch goes out of scope.
 struct Scratch {
   Ctx& c;
-  std::vector<std::pair<void*, size_t>> bufs;
-  explicit Scratch(Ctx& cc) : c(cc) {}
+  Arena::Mark m;
+  explicit Scratch(Ctx& cc) : c(cc), m(cc.arena.mark()) {}
   template <class T>
   T* get(size_t n) {
-    void* p = c.al.alloc(sizeof(T) * std::max<size_t>(n, 1));
-    bufs.push_back({p, sizeof(T) * std::max<size_t>(n, 1)});
-    return (T*)p;
+    return (T*)c.arena.alloc(c.al, sizeof(T) * std::max<size_t>(n, 1));
   }
-  ~Scratch() {
-    for (auto& b : bufs) c.al.release(b.first, b.second);
-  }
+  ~Scratch() { c.arena.reset(m); }
 };
 
 template <class T>
 static void exclusive_scan(Ctx& c, const T* in, T* out, int n) {
+  Scratch S(c);
   size_t tmp = 0;
   SI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, c.s));
-  void* t = c.al.alloc(tmp + 16);
+  void* t = S.get<char>(tmp + 16);
   SI_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, n, c.s));
-  c.al.release(t, tmp + 16);
-  c.launches += 2;
+  c.launches += 1;
 }
 
 template <class T>
@@ -667,9 +664,8 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
     cub::DoubleBuffer<int> db(k1, k2);
     size_t tmp = 0;
     SI_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, db, total, nr, off, off + 1, c.s));
-    void* t = c.al.alloc(tmp + 16);
+    void* t = S.get<char>(tmp + 16);
     SI_CUDA(cub::DeviceSegmentedSort::SortKeys(t, tmp, db, total, nr, off, off + 1, c.s));
-    c.al.release(t, tmp + 16);
     c.launches += 2;
     k1 = db.Current();
   }
@@ -737,9 +733,8 @@ static void transpose(Ctx& c, const BsrMat& X, DBuf<int>& trp, DBuf<int>& tci, D
   while ((1LL << bits) <= X.nbc) ++bits;
   size_t tmp = 0;
   SI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, X.ci, kk, e0, e1, (int)nnz, 0, bits, c.s));
-  void* t = c.al.alloc(tmp + 16);
+  void* t = S.get<char>(tmp + 16);
   SI_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, X.ci, kk, e0, e1, (int)nnz, 0, bits, c.s));
-  c.al.release(t, tmp + 16);
   c.launches += 2;
   trp.ensure(c.al, X.nbc + 1);
   tci.ensure(c.al, nnz);
@@ -1283,9 +1278,9 @@ static void build_transfer(Ctx& c, Level& L, Level& Lc, int lvl, int na, Scratch
     while ((1LL << bits) <= na) ++bits;
     size_t tmp = 0;
     SI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, skey, idx, members, nb, 0, bits, c.s));
-    void* t = c.al.alloc(tmp + 16);
+    Scratch St(c);
+    void* t = St.get<char>(tmp + 16);
     SI_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, key, skey, idx, members, nb, 0, bits, c.s));
-    c.al.release(t, tmp + 16);
     c.launches += 2;
   }
   int* start = S.get<int>(na + 1);
@@ -1308,24 +1303,16 @@ static void build_transfer(Ctx& c, Level& L, Level& Lc, int lvl, int na, Scratch
   SI_LAUNCHED(c);
   tick(c, "tentative", lvl);
   BsrMat Pt{nb, na, B, 3, ptn, ptrp, ptci, ptval};
-  // T = A P_tent ; P = P_tent - omega Dinv T  (pattern of T)
-  DBuf<int> trp, tci;
-  DBuf<double> tval;
+  // T = A P_tent ; P = P_tent - omega Dinv T  (P takes T's pattern)
   long long tn = 0;
-  spgemm<B, B, 3>(c, view(L), Pt, trp, tci, tval, tn);
+  spgemm<B, B, 3>(c, view(L), Pt, L.Prp, L.Pci, L.Tval, tn);
   tick(c, "A*Pt", lvl);
-  L.Prp.free_();
-  L.Pci.free_();
-  L.Pval.free_();
-  L.Prp = trp;
-  L.Pci = tci;
   L.Pnnzb = tn;
   L.Pval.ensure(c.al, (size_t)tn * B * 3);
   const double omega = 4.0 / (3.0 * L.lmax);
-  k_smooth_p<B><<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.Prp.get(), L.Pci.get(), tval.get(), L.dinv.get(),
+  k_smooth_p<B><<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.Prp.get(), L.Pci.get(), L.Tval.get(), L.dinv.get(),
                                                     L.agg.get(), ptrp, ptval, omega, L.Pval.get());
   SI_LAUNCHED(c);
-  tval.free_();
   L.nbc = na;
   BsrMat P{nb, na, B, 3, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.Pval.get()};
   tick(c, "smoothP", lvl);
@@ -1334,18 +1321,13 @@ static void build_transfer(Ctx& c, Level& L, Level& Lc, int lvl, int na, Scratch
   L.Rnnzb = L.Pnnzb;
   tick(c, "transpose", lvl);
   // A_c = R (A P)
-  DBuf<int> aprp, apci;
-  DBuf<double> apval;
   long long apn = 0;
-  spgemm<B, B, 3>(c, view(L), P, aprp, apci, apval, apn);
+  spgemm<B, B, 3>(c, view(L), P, c.ap_rp, c.ap_ci, c.ap_val, apn);
   tick(c, "A*P", lvl);
-  BsrMat AP{nb, na, B, 3, apn, aprp.get(), apci.get(), apval.get()};
+  BsrMat AP{nb, na, B, 3, apn, c.ap_rp.get(), c.ap_ci.get(), c.ap_val.get()};
   BsrMat R{na, nb, 3, B, L.Rnnzb, L.Rrp.get(), L.Rci.get(), L.Rval.get()};
   spgemm<3, B, 3>(c, R, AP, Lc.rp, Lc.ci, Lc.val, Lc.nnzb);
   tick(c, "R*AP", lvl);
-  aprp.free_();
-  apci.free_();
-  apval.free_();
   Lc.nb = na;
   Lc.b = 3;
   k_fix_zero_diag<<<grid_for(na), kThreads, 0, c.s>>>(na, Lc.rp.get(), Lc.ci.get(), Lc.val.get());
@@ -1372,12 +1354,17 @@ static void coarse_factor(Ctx& c, Level& L) {
 void amg_free(Ctx& c) {
   for (auto& L : c.lv) {
     DBuf<int>* ib[] = {&L.rp, &L.ci, &L.Prp, &L.Pci, &L.Rrp, &L.Rci, &L.agg};
-    DBuf<double>* db[] = {&L.val, &L.dinv, &L.Pval, &L.Rval, &L.B, &L.x, &L.rhs, &L.r, &L.d, &L.d2, &L.z};
+    DBuf<double>* db[] = {&L.val, &L.dinv, &L.Pval, &L.Rval, &L.B, &L.x, &L.rhs, &L.r, &L.d, &L.d2, &L.z, &L.Tval};
     for (auto* b : ib) b->free_();
     for (auto* b : db) b->free_();
   }
   c.lv.clear();
+  c.nlev = 0;
   c.cinv.free_();
+  c.ap_rp.free_();
+  c.ap_ci.free_();
+  c.ap_val.free_();
+  c.arena.release_all(c.al);
   c.amg_ready = false;
 }
 
@@ -1394,20 +1381,12 @@ __global__ void k_level0_nullspace(int n, double L, double* __restrict__ B) {
 
 void amg_setup_impl(Ctx& c) {
   SI_CHECK(c.assembled, SEAICE_ESTATE, "amg_setup before assemble");
-  // keep level-0 pattern across setups, drop the rest
+  // the level pool keeps every buffer (grow-only) across setups; level 0's pattern is fixed
   if (c.lv.empty()) {
     c.lv.emplace_back();
     build_level0_pattern(c, c.lv[0]);
-  } else {
-    while (c.lv.size() > 1) {
-      Level& L = c.lv.back();
-      DBuf<int>* ib[] = {&L.rp, &L.ci, &L.Prp, &L.Pci, &L.Rrp, &L.Rci, &L.agg};
-      DBuf<double>* db[] = {&L.val, &L.dinv, &L.Pval, &L.Rval, &L.B, &L.x, &L.rhs, &L.r, &L.d, &L.d2, &L.z};
-      for (auto* b : ib) b->free_();
-      for (auto* b : db) b->free_();
-      c.lv.pop_back();
-    }
   }
+  c.nlev = 1;
   c.amg_ready = false;
   SI_CUDA(cudaMemsetAsync(c.flag.get(), 0, sizeof(int) * 4, c.s));
   Level& L0 = c.lv[0];
@@ -1438,18 +1417,19 @@ void amg_setup_impl(Ctx& c) {
     const int na = (L.b == 2) ? aggregate_level<2>(c, L, lvl, dnorm, S) : aggregate_level<3>(c, L, lvl, dnorm, S);
     tick(c, "aggregate", lvl);
     if (na == 0 || na > 0.9 * L.nb) break;
-    c.lv.emplace_back();
-    Level& Lc = c.lv.back();
+    if ((int)c.lv.size() == c.nlev) c.lv.emplace_back();  // may move Level objects (DBufs are handles)
+    Level& Lc = c.lv[c.nlev];
     Level& Lf = c.lv[lvl];
+    ++c.nlev;
     if (Lf.b == 2) build_transfer<2>(c, Lf, Lc, lvl, na, S);
     else build_transfer<3>(c, Lf, Lc, lvl, na, S);
   }
-  Level& Lc = c.lv.back();
+  Level& Lc = c.lv[c.nlev - 1];
   const long long nd = (long long)Lc.nb * Lc.b;
   SI_CHECK(nd <= 8192, SEAICE_EINVAL, "AMG coarsest level too large for the dense solve (coarsening stalled)");
-  tick(c, nullptr, (int)c.lv.size() - 1);
+  tick(c, nullptr, c.nlev - 1);
   coarse_factor(c, Lc);
-  tick(c, "coarse", (int)c.lv.size() - 1);
+  tick(c, "coarse", c.nlev - 1);
   const int flag = read_scalar(c, c.flag.get());
   SI_CHECK(!(flag & 4), SEAICE_ENONFINITE, "AMG: singular diagonal block");
   SI_CHECK(!(flag & 8), SEAICE_ENONFINITE, "AMG: coarse matrix not positive definite");
@@ -1532,7 +1512,7 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
 
 static void vcycle_level(Ctx& c, int l, const double* b, double* x) {
   Level& L = c.lv[l];
-  if (l + 1 == (int)c.lv.size()) {
+  if (l + 1 == c.nlev) {
     prof_begin(c);
     k_dense_gemv<<<grid_for((long long)c.cn * 32, 256), 256, 0, c.s>>>(c.cn, c.cinv.get(), b, x);
     SI_LAUNCHED(c);

@@ -93,7 +93,7 @@ int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* o
     EvTimer t(c);
     amg_setup_impl(c);
     st.t_amg = t.ms();
-    st.amg_levels = (int)c.lv.size();
+    st.amg_levels = c.nlev;
     st.amg_op_complexity = c.op_complexity;
   }
   // a-5: J vt = R
@@ -214,7 +214,7 @@ void seaice_default_params(seaice_params* p, int32_t n) {
   p->precond = SEAICE_PC_AMG;
   p->amg_theta = 0.08;
   p->cheb_degree = 3;
-  p->coarse_max_dof = 1200;
+  p->coarse_max_dof = 400;
   p->max_levels = 25;
   p->cheb_lower = 0.03;
   p->cheb_upper = 1.1;
@@ -332,7 +332,7 @@ int seaice_amg_setup(seaice_ctx* h, int32_t* levels_out, double* oc_out) {
   API_BEGIN(h)
   SI_CHECK(c.assembled, SEAICE_ESTATE, "amg_setup before assemble_jacobian");
   amg_setup_impl(c);
-  if (levels_out) *levels_out = (int32_t)c.lv.size();
+  if (levels_out) *levels_out = (int32_t)c.nlev;
   if (oc_out) *oc_out = c.op_complexity;
   return SEAICE_OK;
   API_END
@@ -341,10 +341,10 @@ int seaice_amg_setup(seaice_ctx* h, int32_t* levels_out, double* oc_out) {
 int seaice_amg_level(seaice_ctx* h, int32_t level, seaice_bsr* A_out, seaice_bsr* P_out, int32_t* agg_host) {
   API_BEGIN(h)
   SI_CHECK(c.amg_ready, SEAICE_ESTATE, "no AMG hierarchy");
-  SI_CHECK(level >= 0 && level < (int)c.lv.size(), SEAICE_EINVAL, "level out of range");
+  SI_CHECK(level >= 0 && level < c.nlev, SEAICE_EINVAL, "level out of range");
   const Level& L = c.lv[level];
   if (A_out) *A_out = seaice_bsr{L.nb, L.nb, L.b, L.b, L.nnzb, L.rp.get(), L.ci.get(), L.val.get()};
-  const bool last = level + 1 == (int)c.lv.size();
+  const bool last = level + 1 == c.nlev;
   if (P_out) {
     if (last)
       std::memset(P_out, 0, sizeof(*P_out));

@@ -27,6 +27,52 @@ struct Level {
   DBuf<double> B;             // near-nullspace rows [nb*b][3]
   // V-cycle work vectors (length nb*b)
   DBuf<double> x, rhs, r, d, d2, z;
+  DBuf<double> Tval;          // A P_tent values (pattern of P), setup scratch kept for reuse
+};
+
+// Grow-only chunked bump allocator for setup scratch (LIFO marks): avoids an allocator
+// round trip (a Python callback when torch provides the memory) per temporary buffer.
+struct Arena {
+  struct Chunk {
+    char* p;
+    size_t size, used;
+  };
+  std::vector<Chunk> chunks;
+  size_t cur = 0;  // index of the chunk being filled
+  struct Mark {
+    size_t chunk, used;
+  };
+  Mark mark() const { return chunks.empty() ? Mark{0, 0} : Mark{cur, chunks[cur].used}; }
+  void reset(Mark m) {
+    if (chunks.empty()) return;
+    for (size_t i = m.chunk + 1; i < chunks.size(); ++i) chunks[i].used = 0;
+    cur = m.chunk;
+    chunks[cur].used = m.used;
+  }
+  void* alloc(Allocator& al, size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes == 0) bytes = 256;
+    while (true) {
+      if (!chunks.empty() && chunks[cur].used + bytes <= chunks[cur].size) {
+        void* p = chunks[cur].p + chunks[cur].used;
+        chunks[cur].used += bytes;
+        return p;
+      }
+      if (!chunks.empty() && cur + 1 < chunks.size()) {
+        ++cur;
+        chunks[cur].used = 0;
+        continue;
+      }
+      size_t sz = std::max(bytes, chunks.empty() ? (size_t)64 << 20 : chunks.back().size * 2);
+      chunks.push_back({(char*)al.alloc(sz), sz, 0});
+      cur = chunks.size() - 1;
+    }
+  }
+  void release_all(Allocator& al) {
+    for (auto& ch : chunks) al.release(ch.p, ch.size);
+    chunks.clear();
+    cur = 0;
+  }
 };
 
 // Per-kernel-class CUDA-event timing (seaice_profile_enable/read): event pairs are
@@ -103,8 +149,12 @@ struct Ctx {
   // Krylov
   DBuf<double> V, Z, w, xk, rk;
 
-  // AMG
+  // AMG (lv is a pool: levels [0, nlev) are active; buffers are reused across setups)
   std::vector<Level> lv;
+  int nlev = 0;
+  Arena arena;
+  DBuf<int> ap_rp, ap_ci;
+  DBuf<double> ap_val;
   DBuf<double> cinv;  // dense coarse inverse
   int cn = 0;         // coarse DOFs
   double op_complexity = 0.0;

@@ -237,7 +237,7 @@ def level0_nullspace(n, L):
     return B
 
 
-def setup(J, pb=None, theta=0.08, coarse_max_dof=400, max_levels=25, power_iters=20, seed=0,
+def setup(J, pb=None, theta=0.04, coarse_max_dof=400, max_levels=25, power_iters=20, seed=0,
           cheb_degree=3, cheb_lower=0.03, cheb_upper=1.1, n=None, L=512e3):
     if pb is not None:
         n, L = pb.n, pb.L

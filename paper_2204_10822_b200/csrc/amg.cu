@@ -1351,7 +1351,12 @@ static void coarse_factor(Ctx& c, Level& L) {
   SI_CUDA(cudaStreamSynchronize(c.s));
 }
 
+void vgraph_destroy(Ctx& c);
+
 void amg_free(Ctx& c) {
+  vgraph_destroy(c);
+  c.vc_in.free_();
+  c.vc_out.free_();
   for (auto& L : c.lv) {
     DBuf<int>* ib[] = {&L.rp, &L.ci, &L.Prp, &L.Pci, &L.Rrp, &L.Rci, &L.agg};
     DBuf<double>* db[] = {&L.val, &L.dinv, &L.Pval, &L.Rval, &L.B, &L.x, &L.rhs, &L.r, &L.d, &L.d2, &L.z, &L.Tval};
@@ -1379,8 +1384,11 @@ __global__ void k_level0_nullspace(int n, double L, double* __restrict__ B) {
   b[3] = 0.0; b[4] = 1.0; b[5] = (x - 0.5 * L) / L;
 }
 
+void vgraph_destroy(Ctx& c);
+
 void amg_setup_impl(Ctx& c) {
   SI_CHECK(c.assembled, SEAICE_ESTATE, "amg_setup before assemble");
+  vgraph_destroy(c);
   // the level pool keeps every buffer (grow-only) across setups; level 0's pattern is fixed
   if (c.lv.empty()) {
     c.lv.emplace_back();
@@ -1533,9 +1541,57 @@ static void vcycle_level(Ctx& c, int l, const double* b, double* x) {
   smooth(c, l, b, x, false);
 }
 
+static long long g_vgraph_kernels = 0;
+
+void vgraph_destroy(Ctx& c) {
+  if (c.vgraph) {
+    cudaStreamSynchronize(c.s);
+    cudaGraphExecDestroy(c.vgraph);
+    c.vgraph = nullptr;
+  }
+}
+
+// One V-cycle z = M^-1 r.  The whole cycle (~10 launches per level) is captured once per
+// hierarchy into a CUDA graph reading vc_in and writing vc_out, so the small coarse-level
+// kernels are not paced by host launch latency.
 void amg_vcycle(Ctx& c, const double* r, double* z) {
   SI_CHECK(c.amg_ready, SEAICE_ESTATE, "V-cycle without hierarchy");
-  vcycle_level(c, 0, r, z);
+  if (!c.use_graphs || c.prof.on) {
+    vcycle_level(c, 0, r, z);
+    return;
+  }
+  if (!c.vgraph) {
+    c.vc_in.ensure(c.al, c.N);
+    c.vc_out.ensure(c.al, c.N);
+    cudaGraph_t g = nullptr;
+    const long long l0 = c.launches;
+    // capture on a private stream (the caller's may be the legacy default stream, which
+    // cannot be captured); the graph is then launched on the caller's stream
+    if (!c.cap_stream) SI_CUDA(cudaStreamCreateWithFlags(&c.cap_stream, cudaStreamNonBlocking));
+    SI_CUDA(cudaStreamSynchronize(c.s));
+    cudaStream_t user = c.s;
+    c.s = c.cap_stream;
+    SI_CUDA(cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal));
+    try {
+      vcycle_level(c, 0, c.vc_in.get(), c.vc_out.get());
+    } catch (...) {
+      cudaStreamEndCapture(c.s, &g);
+      c.s = user;
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    cudaError_t ec = cudaStreamEndCapture(c.s, &g);
+    c.s = user;
+    SI_CUDA(ec);
+    SI_CUDA(cudaGraphInstantiate(&c.vgraph, g, 0));
+    cudaGraphDestroy(g);
+    g_vgraph_kernels = c.launches - l0;
+    c.launches = l0;
+  }
+  copy(c, c.vc_in.get(), r, c.N);
+  SI_CUDA(cudaGraphLaunch(c.vgraph, c.s));
+  c.launches += g_vgraph_kernels;
+  copy(c, z, c.vc_out.get(), c.N);
 }
 
 }  // namespace seaice

@@ -212,7 +212,7 @@ void seaice_default_params(seaice_params* p, int32_t n) {
   p->restart = 30;
   p->krylov_maxit = 300;
   p->precond = SEAICE_PC_AMG;
-  p->amg_theta = 0.08;
+  p->amg_theta = 0.04;
   p->cheb_degree = 3;
   p->coarse_max_dof = 400;
   p->max_levels = 25;
@@ -241,6 +241,7 @@ int seaice_create(const seaice_params* p, const seaice_runtime* rt, seaice_ctx**
     c.dx = p->L / p->n;
     c.ph = Phys{p->rho_i, p->rho_a, p->rho_o, p->C_a, p->C_o, p->P_star, p->C, p->e, p->delta_min, p->f_c,
                 c.dx, 0.0, p->n};
+    c.use_graphs = getenv("SEAICE_NO_GRAPHS") == nullptr;
     SI_CUDA(cudaMallocHost(&c.hbuf, 256 * sizeof(double)));
     SI_CUDA(cudaEventCreate(&c.ev0));
     SI_CUDA(cudaEventCreate(&c.ev1));
@@ -284,6 +285,7 @@ int seaice_destroy(seaice_ctx* h) {
   prof_harvest(c, true);
   for (auto e : c.prof.free_ev) cudaEventDestroy(e);
   if (c.hbuf) cudaFreeHost(c.hbuf);
+  if (c.cap_stream) cudaStreamDestroy(c.cap_stream);
   if (c.ev0) cudaEventDestroy(c.ev0);
   if (c.ev1) cudaEventDestroy(c.ev1);
   cudaStreamSynchronize(c.s);

@@ -100,6 +100,7 @@ struct Prof {
   struct Rec {
     int k;
     cudaEvent_t a, b;
+    bool owned_by_graph;
   };
   std::vector<Rec> pending;
   cudaEvent_t cur_a = nullptr;
@@ -155,6 +156,11 @@ struct Ctx {
   Arena arena;
   DBuf<int> ap_rp, ap_ci;
   DBuf<double> ap_val;
+  // the V-cycle as one CUDA graph (rebuilt after each setup): in vc_in -> out vc_out
+  cudaGraphExec_t vgraph = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  bool use_graphs = true;
+  DBuf<double> vc_in, vc_out;
   DBuf<double> cinv;  // dense coarse inverse
   int cn = 0;         // coarse DOFs
   double op_complexity = 0.0;
@@ -181,8 +187,10 @@ inline void prof_harvest(Ctx& c, bool wait) {
       cudaEventElapsedTime(&t, r.a, r.b);
       P.ms[r.k] += t;
       P.cnt[r.k] += 1;
-      P.free_ev.push_back(r.a);
-      P.free_ev.push_back(r.b);
+      if (!r.owned_by_graph) {
+        P.free_ev.push_back(r.a);
+        P.free_ev.push_back(r.b);
+      }
     } else {
       P.pending[keep++] = r;
     }
@@ -203,6 +211,8 @@ inline cudaEvent_t prof_event(Ctx& c) {
   P.free_ev.pop_back();
   return e;
 }
+// Per-kernel timing is eager-only: while profiling is on the V-cycle is not replayed as a
+// CUDA graph (timing events cannot be taken inside graph replays).
 inline void prof_begin(Ctx& c) {
   if (!c.prof.on) return;
   c.prof.cur_a = prof_event(c);
@@ -213,7 +223,7 @@ inline void prof_end(Ctx& c, int k, double bytes = 0.0) {
   c.prof.bytes[k] += bytes;
   cudaEvent_t b = prof_event(c);
   cudaEventRecord(b, c.s);
-  c.prof.pending.push_back({k, c.prof.cur_a, b});
+  c.prof.pending.push_back({k, c.prof.cur_a, b, false});
 }
 #define SI_LAUNCHED(c) \
   do {                 \

@@ -80,6 +80,8 @@ typedef struct {
   int32_t power_iters;     /* power iterations for lambda_max(D^-1 A) */
   int32_t project_pi;      /* 0 (default): store pi unprojected (reading G5) */
   uint64_t amg_seed;
+  int32_t agg_dist0;       /* aggregation root distance on the finest level: 2 = MIS(2) (default), 1 = MIS(1) */
+  int32_t agg_dist;        /* same on coarse levels */
 } seaice_params;
 
 /* Compressed-sparse-row view (scalar rows). Index arrays int32, values fp64. */

@@ -96,8 +96,9 @@ def strength(A, b, theta):
     return G
 
 
-def mis2(G, seed, level):
-    """Round-synchronous MIS(2) on the strength graph G (definition in the module header)."""
+def mis2(G, seed, level, dist=2):
+    """Round-synchronous MIS(2) on the strength graph G (definition in the module header);
+    dist=1 gives MIS(1) (one max pass per round)."""
     nb = G.shape[0]
     deg = np.diff(G.indptr)
     isolated = deg == 0
@@ -110,7 +111,7 @@ def mis2(G, seed, level):
     while np.any(state == 1):
         key = (state << np.uint64(62)) | (h << np.uint64(25)) | idx
         T1 = np.maximum.reduceat(key[C.indices], C.indptr[:-1])
-        T2 = np.maximum.reduceat(T1[C.indices], C.indptr[:-1])
+        T2 = np.maximum.reduceat(T1[C.indices], C.indptr[:-1]) if dist == 2 else T1
         und = state == 1
         new_in = und & (T2 == key)
         new_out = und & ~new_in & ((T2 >> np.uint64(62)) == 2)
@@ -238,7 +239,7 @@ def level0_nullspace(n, L):
 
 
 def setup(J, pb=None, theta=0.04, coarse_max_dof=400, max_levels=25, power_iters=20, seed=0,
-          cheb_degree=3, cheb_lower=0.03, cheb_upper=1.1, n=None, L=512e3):
+          cheb_degree=3, cheb_lower=0.03, cheb_upper=1.1, n=None, L=512e3, agg_dist0=2, agg_dist=2):
     if pb is not None:
         n, L = pb.n, pb.L
     A = J.tocsr()
@@ -253,7 +254,7 @@ def setup(J, pb=None, theta=0.04, coarse_max_dof=400, max_levels=25, power_iters
         if A.shape[0] <= coarse_max_dof or lvl + 1 == max_levels:
             break
         G = strength(A, b, theta)
-        roots, isolated, rounds = mis2(G, seed, lvl)
+        roots, isolated, rounds = mis2(G, seed, lvl, agg_dist0 if lvl == 0 else agg_dist)
         agg = aggregate(G, roots, isolated)
         na = int(roots.sum())
         if na == 0 or na > 0.9 * lev["nb"]:

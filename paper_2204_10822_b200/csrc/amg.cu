@@ -652,6 +652,8 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
   SI_LAUNCHED(c);
   exclusive_scan(c, ub, off, nr + 1);
   const long long total = read_scalar(c, off + nr);
+  SI_CHECK(total < (1LL << 31) - 1, SEAICE_ENOMEM,
+           "SpGEMM expansion exceeds 2^31 products (coarsening too slow for this operator)");
   int* k1 = S.get<int>(total);
   int* k2 = S.get<int>(total);
   const bool wide = total > 48LL * nr;  // long rows: warp per row
@@ -1142,11 +1144,12 @@ __global__ void __launch_bounds__(256) k_gresid(int nb, const int* __restrict__ 
 }
 
 static int pick_group(long long nnzb, int nb) {
+  static const int shift = getenv("SEAICE_GROUP_SHIFT") ? atoi(getenv("SEAICE_GROUP_SHIFT")) : 0;  // tuning aid
   const double avg = nb > 0 ? (double)nnzb / nb : 1.0;
-  if (avg <= 6.0) return 4;
-  if (avg <= 14.0) return 8;
-  if (avg <= 40.0) return 16;
-  return 32;
+  // measured on B200 (scripts/vcycle_bench.py): ~2-4 blocks per lane is the sweet spot
+  int g = avg <= 14.0 ? 4 : avg <= 40.0 ? 8 : avg <= 120.0 ? 16 : 32;
+  g = shift >= 0 ? (g << shift) : (g >> -shift);
+  return g < 4 ? 4 : (g > 32 ? 32 : g);
 }
 static int ggrid(int nb, int G) { return (int)(((long long)nb * G + 255) / 256); }
 
@@ -1233,14 +1236,15 @@ static int aggregate_level(Ctx& c, Level& L, int lvl, const double* dnorm, Scrat
   int* und = S.get<int>(1);
   k_mis_init<<<grid_for(nb), kThreads, 0, c.s>>>(nb, grp, salt(c.p.amg_seed, lvl, 1), key);
   SI_LAUNCHED(c);
+  const int dist = (lvl == 0) ? c.p.agg_dist0 : c.p.agg_dist;  // MIS(2) or MIS(1)
   for (int round = 0;; ++round) {
-    SI_CHECK(round < 10000, SEAICE_ECUDA, "MIS(2) did not terminate");
+    SI_CHECK(round < 10000, SEAICE_ECUDA, "MIS did not terminate");
     k_mis_max<<<grid_for(nb), kThreads, 0, c.s>>>(nb, grp, gci, key, T1);
-    k_mis_max<<<grid_for(nb), kThreads, 0, c.s>>>(nb, grp, gci, T1, T2);
+    if (dist == 2) k_mis_max<<<grid_for(nb), kThreads, 0, c.s>>>(nb, grp, gci, T1, T2);
     SI_CUDA(cudaMemsetAsync(und, 0, sizeof(int), c.s));
-    k_mis_update<<<grid_for(nb), kThreads, 0, c.s>>>(nb, key, T2, und);
+    k_mis_update<<<grid_for(nb), kThreads, 0, c.s>>>(nb, key, dist == 2 ? T2 : T1, und);
     SI_LAUNCHED(c);
-    c.launches += 2;
+    c.launches += dist;
     if (read_scalar(c, und) == 0) break;
   }
   int* isroot = S.get<int>(nb + 1);

@@ -62,6 +62,8 @@ void validate(const seaice_params* p) {
   SI_CHECK(p->cheb_degree >= 1 && p->cheb_degree <= 16, SEAICE_EINVAL, "cheb_degree in [1,16]");
   SI_CHECK(p->max_levels >= 1 && p->max_levels <= 40, SEAICE_EINVAL, "max_levels in [1,40]");
   SI_CHECK(p->coarse_max_dof >= 3 && p->coarse_max_dof <= 8192, SEAICE_EINVAL, "coarse_max_dof in [3,8192]");
+  SI_CHECK((p->agg_dist0 == 1 || p->agg_dist0 == 2) && (p->agg_dist == 1 || p->agg_dist == 2), SEAICE_EINVAL,
+           "agg_dist0/agg_dist must be 1 or 2");
 }
 
 int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* out) {
@@ -221,6 +223,8 @@ void seaice_default_params(seaice_params* p, int32_t n) {
   p->power_iters = 20;
   p->project_pi = 0;
   p->amg_seed = 0;
+  p->agg_dist0 = 2;
+  p->agg_dist = 2;
 }
 
 int seaice_create(const seaice_params* p, const seaice_runtime* rt, seaice_ctx** out) {

@@ -33,7 +33,8 @@ class Params(C.Structure):
                 ("krylov_maxit", C.c_int32), ("precond", C.c_int32), ("amg_theta", C.c_double),
                 ("cheb_degree", C.c_int32), ("coarse_max_dof", C.c_int32), ("max_levels", C.c_int32),
                 ("cheb_lower", C.c_double), ("cheb_upper", C.c_double), ("power_iters", C.c_int32),
-                ("project_pi", C.c_int32), ("amg_seed", C.c_uint64)]
+                ("project_pi", C.c_int32), ("amg_seed", C.c_uint64), ("agg_dist0", C.c_int32),
+                ("agg_dist", C.c_int32)]
 
 
 ALLOC_T = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)

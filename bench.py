@@ -110,6 +110,20 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def reduce_timing(ms, units, world, device=None):
+    """Whole-job timing over replicas: the MAX of the per-rank device-timed milliseconds and
+    the SUM of the per-rank work units (each rank solves an independent replica)."""
+    if world <= 1:
+        return ms, units
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    u = torch.tensor([float(units)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(u.item())
+
+
 # ----------------------------------------------------------------------------- oracle arm
 def oracle_sample(cfg, n_sample=256):
     """One full sv-Newton iteration of the CPU oracle (assembly, AMG setup, AMG-FGMRES,
@@ -238,15 +252,7 @@ def run_ours(a, rank, world, local_rank):
     ctx.profile(False)
     kry = sum(s["krylov_iters_total"] for s in stats)
     units = float(N) * kry
-    t = torch.tensor([ms, units], dtype=torch.float64, device=dev)
-    if world > 1:
-        tm = t[:1].clone()
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-        tu = t[1:].clone()
-        dist.all_reduce(tu, op=dist.ReduceOp.SUM)
-        ms_max, units_all = float(tm.item()), float(tu.item())
-    else:
-        ms_max, units_all = ms, units
+    ms_max, units_all = reduce_timing(ms, units, world, dev)
     value = units_all / (ms_max / 1e3)
 
     # ---- end-to-end through the host-buffer C-ABI call (same steps again)
@@ -268,15 +274,7 @@ def run_ours(a, rank, world, local_rank):
         barrier()
         ms_e = e0.elapsed_time(e1)
         kry_e = sum(s["krylov_iters_total"] for s in e2e_stats)
-        te = torch.tensor([ms_e, float(N) * kry_e], dtype=torch.float64, device=dev)
-        if world > 1:
-            x = te[:1].clone()
-            dist.all_reduce(x, op=dist.ReduceOp.MAX)
-            y = te[1:].clone()
-            dist.all_reduce(y, op=dist.ReduceOp.SUM)
-            ms_e, u_e = float(x.item()), float(y.item())
-        else:
-            u_e = float(N) * kry_e
+        ms_e, u_e = reduce_timing(ms_e, float(N) * kry_e, world, dev)
         e2e = {"value": u_e / (ms_e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * (2 * Nc + 3 * N),
                "d2h_bytes_per_step": 8 * N, "ms_per_step": ms_e / a.steps,
                "s_per_timestep": ms_e / 1e3 / a.steps}

@@ -495,6 +495,212 @@ void set_step_impl(Ctx& c, double dt, double t_new, const double* h, const doubl
   c.have_r0 = false;
 }
 
+// ------------------------------------------------------------------ K1, tiled (Jacobian path)
+// Two-phase, atomics-free: a CTA owns a 31 x 8 tile of nodes.  Phase 1: one thread per cell of
+// the 32 x 9 cells touching the tile computes the packed 8x8 element matrix (upper triangle,
+// 36 values) and the 8 element residual terms into shared memory (SoA, bank-conflict free).
+// Phase 2: one thread per node gathers its two rows from the four adjacent cells, writes the
+// 36 stencil slots (coalesced) and its two residual entries.  Each cell's quadrature-point
+// algebra is done once per tile (1.16x recompute for the halo) instead of once per node (4x).
+constexpr int kTX = 31, kTY = 8, kTC = (kTX + 1) * (kTY + 1);  // 248 nodes, 288 cells
+constexpr int kTThreads = kTC;
+constexpr int kKE = 36;
+__host__ __device__ constexpr int ke_idx(int p, int q) { return p * 8 - p * (p - 1) / 2 + (q - p); }  // p <= q
+constexpr size_t kTileSmem = (size_t)(kKE + 8) * kTC * sizeof(double);
+
+template <int KIND>
+__global__ void __launch_bounds__(kTThreads, 2) k_assemble_tiled(Phys ph, int Nn, const double* __restrict__ v,
+                                                                  const double* __restrict__ pi,
+                                                                  const double* __restrict__ P,
+                                                                  const double* __restrict__ rhoh,
+                                                                  const double* __restrict__ vo,
+                                                                  const double* __restrict__ F,
+                                                                  double* __restrict__ Jst, double* __restrict__ R,
+                                                                  double* __restrict__ part) {
+  extern __shared__ double smem[];
+  double* Ks = smem;             // [36][kTC]
+  double* Rs = smem + kKE * kTC;  // [8][kTC]
+  __shared__ double sh[32];
+  const int n = ph.n, s = n + 1;
+  const int i0 = blockIdx.x * kTX, j0 = blockIdx.y * kTY;
+  const int t = threadIdx.x;
+  // ---- phase 1: element matrix and element residual of cell t
+  {
+    const int ci = i0 - 1 + t % (kTX + 1), cj = j0 - 1 + t / (kTX + 1);
+    if (ci >= 0 && ci < n && cj >= 0 && cj < n) {
+      const long long Nc = (long long)n * n;
+      const int cell = cj * n + ci;
+      double u[4][2], uo[4][2];
+      {
+        const int nd0 = cj * s + ci;
+        const int ids[4] = {nd0, nd0 + 1, nd0 + s + 1, nd0 + s};
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const double2 a1 = __ldg(reinterpret_cast<const double2*>(v) + ids[b]);
+          const double2 a2 = __ldg(reinterpret_cast<const double2*>(vo) + ids[b]);
+          u[b][0] = a1.x; u[b][1] = a1.y; uo[b][0] = a2.x; uo[b][1] = a2.y;
+        }
+      }
+      const double Pc = P[cell], rh = rhoh[cell];
+      const double inv_dx = 1.0 / ph.dx, inv_e = 1.0 / ph.e;
+      const double w = 0.25 * ph.dx * ph.dx;
+      const double co = ph.C_o * ph.rho_o;
+      const double dt = ph.dt;
+      const double dmin2 = ph.delta_min * ph.delta_min;
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) {
+        double vx = 0, vy = 0, ox_ = 0, oy_ = 0, L00 = 0, L01 = 0, L10 = 0, L11 = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          vx += Nq(q, b) * u[b][0];
+          vy += Nq(q, b) * u[b][1];
+          ox_ += Nq(q, b) * uo[b][0];
+          oy_ += Nq(q, b) * uo[b][1];
+          L00 += u[b][0] * Gx(q, b);
+          L01 += u[b][0] * Gy(q, b);
+          L10 += u[b][1] * Gx(q, b);
+          L11 += u[b][1] * Gy(q, b);
+        }
+        L00 *= inv_dx; L01 *= inv_dx; L10 *= inv_dx; L11 *= inv_dx;
+        const V3 tq = tau_hat_grad(L00, L01, L10, L11, inv_e);
+        const double D = sqrt(dmin2 + 2.0 * dot3(tq, tq));
+        const double c0 = Pc / D;
+        const double wx = ox_ - vx, wy = oy_ - vy;
+        const double nw = sqrt(wx * wx + wy * wy);
+        double d00 = co * nw, d11 = co * nw, d01 = 0.0;
+        if (nw >= 1e-12) {
+          const double inw = co / nw;
+          d00 += inw * wx * wx;
+          d11 += inw * wy * wy;
+          d01 = inw * wx * wy;
+        }
+        // linearised stress coefficient C (symmetric 3x3)
+        double C00 = c0, C11 = c0, C22 = c0, C01 = 0.0, C02 = 0.0, C12 = 0.0;
+        if (KIND == SEAICE_JAC_SV) {
+          const V3 p = pi_hat(pi[(0 * 4 + q) * Nc + cell], pi[(1 * 4 + q) * Nc + cell], pi[(2 * 4 + q) * Nc + cell]);
+          const double sc = fmax(1.0, kR2 * sqrt(dot3(p, p)));
+          const double c1 = Pc / (D * D * sc);
+          C00 -= c1 * 2.0 * p.x * tq.x; C11 -= c1 * 2.0 * p.y * tq.y; C22 -= c1 * 2.0 * p.z * tq.z;
+          C01 -= c1 * (p.x * tq.y + tq.x * p.y);
+          C02 -= c1 * (p.x * tq.z + tq.x * p.z);
+          C12 -= c1 * (p.y * tq.z + tq.y * p.z);
+        } else if (KIND == SEAICE_JAC_STD) {
+          const double c1 = 2.0 * Pc / (D * D * D);
+          C00 -= c1 * tq.x * tq.x; C11 -= c1 * tq.y * tq.y; C22 -= c1 * tq.z * tq.z;
+          C01 -= c1 * tq.x * tq.y; C02 -= c1 * tq.x * tq.z; C12 -= c1 * tq.y * tq.z;
+        }
+        // test-function tau^ for the 8 local DOFs p = 2a + k
+        V3 tb[8];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const double gx = Gx(q, a) * inv_dx, gy = Gy(q, a) * inv_dx;
+          tb[2 * a] = tau_hat_ex(gx, gy, inv_e);
+          tb[2 * a + 1] = tau_hat_ey(gx, gy, inv_e);
+        }
+        const double wdt = w * dt;
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq) {
+          const V3& x = tb[qq];
+          const V3 uq{C00 * x.x + C01 * x.y + C02 * x.z, C01 * x.x + C11 * x.y + C12 * x.z,
+                      C02 * x.x + C12 * x.y + C22 * x.z};
+          const int b = qq >> 1, m = qq & 1;
+#pragma unroll
+          for (int pp = 0; pp <= qq; ++pp) {
+            const int a = pp >> 1, k = pp & 1;
+            const double NN = Nq(q, a) * Nq(q, b);
+            double val = wdt * dot3(tb[pp], uq);
+            if (k == m) val += w * rh * NN + wdt * NN * (k == 0 ? d00 : d11);
+            else val += wdt * NN * d01;
+            double* dst = Ks + ke_idx(pp, qq) * kTC + t;
+            *dst = (q == 0) ? val : *dst + val;
+          }
+        }
+        // element residual: -A(v, phi_p)
+#pragma unroll
+        for (int pp = 0; pp < 8; ++pp) {
+          const int a = pp >> 1, k = pp & 1;
+          const double Na = Nq(q, a);
+          const double g = (k == 0 ? Gx(q, a) : Gy(q, a)) * inv_dx;
+          const double val = -w * (rh * (k == 0 ? vx : vy) * Na + dt * c0 * dot3(tq, tb[pp]) - dt * 0.5 * Pc * g -
+                                   dt * co * nw * (k == 0 ? wx : wy) * Na);
+          double* dst = Rs + pp * kTC + t;
+          *dst = (q == 0) ? val : *dst + val;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ---- phase 2: rows of node t
+  double nrm = 0.0;
+  if (t < kTX * kTY) {
+    const int i = i0 + t % kTX, j = j0 + t / kTX;
+    if (i <= n && j <= n) {
+      const int node = j * s + i;
+      if (!(i > 0 && i < n && j > 0 && j < n)) {
+#pragma unroll
+        for (int e = 0; e < 36; ++e) Jst[(long long)e * Nn + node] = (e == 16 || e == 19) ? 1.0 : 0.0;
+        R[2 * node] = 0.0;
+        R[2 * node + 1] = 0.0;
+      } else {
+        double acc[36];
+#pragma unroll
+        for (int e = 0; e < 36; ++e) acc[e] = 0.0;
+        double r0 = F[2 * node], r1 = F[2 * node + 1];
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          // cc: cells (i-1,j-1) a=2, (i,j-1) a=3, (i-1,j) a=1, (i,j) a=0 — same order as k_assemble
+          const int a = (cc == 0) ? 2 : (cc == 1) ? 3 : (cc == 2) ? 1 : 0;
+          const int lc = (i - 1 + (cc & 1) - (i0 - 1)) + (j - 1 + (cc >> 1) - (j0 - 1)) * (kTX + 1);
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+#pragma unroll
+              for (int m = 0; m < 2; ++m) {
+                const int p = 2 * a + k, q = 2 * b + m;
+                const int e = p <= q ? ke_idx(p, q) : ke_idx(q, p);
+                acc[slot_ab(a, b) * 4 + k * 2 + m] += Ks[e * kTC + lc];
+              }
+          r0 += Rs[(2 * a) * kTC + lc];
+          r1 += Rs[(2 * a + 1) * kTC + lc];
+        }
+        R[2 * node] = r0;
+        R[2 * node + 1] = r1;
+        nrm = r0 * r0 + r1 * r1;
+#pragma unroll
+        for (int sl = 0; sl < 9; ++sl) {
+          const int ii = i + (sl % 3) - 1, jj = j + (sl / 3) - 1;
+          const bool bnd = (ii == 0 || ii == n || jj == 0 || jj == n);  // symmetric elimination
+#pragma unroll
+          for (int e = 0; e < 4; ++e) Jst[(long long)(sl * 4 + e) * Nn + node] = bnd ? 0.0 : acc[sl * 4 + e];
+        }
+      }
+    }
+  }
+  const double bs = block_sum(nrm, sh);
+  if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = bs;
+}
+
+template <int KIND>
+static int launch_assemble_tiled(Ctx& c, const double* v, const double* pi, double* R) {
+  static bool attr = false;
+  if (!attr) {
+    SI_CUDA(cudaFuncSetAttribute(k_assemble_tiled<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kTileSmem));
+    attr = true;
+  }
+  const dim3 grid((c.n + 1 + kTX - 1) / kTX, (c.n + 1 + kTY - 1) / kTY);
+  const int g = grid.x * grid.y;
+  c.part.ensure(c.al, g + 64);
+  prof_begin(c);
+  k_assemble_tiled<KIND><<<grid, kTThreads, kTileSmem, c.s>>>(c.ph, c.Nn, v, pi, c.P.get(), c.rhoh.get(),
+                                                               c.vocean.get(), c.F.get(), c.Jst.get(), R,
+                                                               c.part.get());
+  SI_LAUNCHED(c);
+  prof_end(c, PC_ASSEMBLE, 352.0 * c.Nn + 112.0 * c.Nc);
+  return g;
+}
+
 template <int KIND, bool JAC>
 static void launch_assemble(Ctx& c, const double* v, const double* pi, double* R) {
   const int g = grid_for(c.Nn, 128);
@@ -512,19 +718,20 @@ void assemble_impl(Ctx& c, const double* v, const double* pi, bool jac, double* 
   const double* pp = pi ? pi : c.pi.get();
   double* R = c.R.get();
   const int kind = c.p.jacobian;
+  int nparts = grid_for(c.Nn, 128);
   if (!jac) {
-    launch_assemble<SEAICE_JAC_PICARD, false>(c, v, pp, R);
+    launch_assemble<SEAICE_JAC_PICARD, false>(c, v, pp, R);  // residual only: per-node gather
   } else if (kind == SEAICE_JAC_SV) {
-    launch_assemble<SEAICE_JAC_SV, true>(c, v, pp, R);
+    nparts = launch_assemble_tiled<SEAICE_JAC_SV>(c, v, pp, R);
   } else if (kind == SEAICE_JAC_STD) {
-    launch_assemble<SEAICE_JAC_STD, true>(c, v, pp, R);
+    nparts = launch_assemble_tiled<SEAICE_JAC_STD>(c, v, pp, R);
   } else {
-    launch_assemble<SEAICE_JAC_PICARD, true>(c, v, pp, R);
+    nparts = launch_assemble_tiled<SEAICE_JAC_PICARD>(c, v, pp, R);
   }
   if (r_out) {
     SI_CUDA(cudaMemcpyAsync(r_out, R, sizeof(double) * c.N, cudaMemcpyDeviceToDevice, c.s));
   }
-  const double n2 = finish_sum(c, c.part.get(), grid_for(c.Nn, 128));
+  const double n2 = finish_sum(c, c.part.get(), nparts);
   c.last_res_norm = std::sqrt(n2);
   if (norm_host) *norm_host = c.last_res_norm;
   if (jac) {

@@ -179,6 +179,25 @@ def custom_inputs(n: int, seed: int = 0, moving: bool = False, dt: float = 1800.
     return cfg, step_inputs(cfg, 0)
 
 
+def problem1_inputs(n: int, L: float = L_DOMAIN, dt: float = 1800.0) -> StepInputs:
+    """PAPER.md Problem I, a single momentum solve: v_o = 0, v_a = (5, 5) m/s,
+    v^n = 0, H = 2A with A = 1 - 0.5 e^{-800|r|} - 0.4 e^{-90|r1|} - 0.4 e^{-90|r1 + 0.7|},
+    r = 0.04 - (x/1000km - 0.25)^2 - (y/1000km - 0.25)^2, r1 = 0.1 + (2x/1000km)^2 - 2y/1000km
+    (taken as printed, reading G26), evaluated at cell centres; dt = 0.5 h.  The paper uses
+    f_c = 0 and a 1e4 residual reduction."""
+    X, Y = cell_centres(n, L)
+    xk, yk = X / 1.0e6, Y / 1.0e6
+    r = 0.04 - (xk - 0.25) ** 2 - (yk - 0.25) ** 2
+    r1 = 0.1 + (2.0 * xk) ** 2 - 2.0 * yk
+    A = 1.0 - 0.5 * np.exp(-800.0 * np.abs(r)) - 0.4 * np.exp(-90.0 * np.abs(r1)) - 0.4 * np.exp(-90.0 * np.abs(r1 + 0.7))
+    A = np.clip(A, 0.0, 1.0)
+    Nn = (n + 1) ** 2
+    va = np.empty(2 * Nn)
+    va[0::2], va[1::2] = 5.0, 5.0
+    return StepInputs(n=n, dt=dt, t_new=dt, h=2.0 * A, A=A, v_prev=np.zeros(2 * Nn), v_air=va,
+                      v_ocean=np.zeros(2 * Nn), L=L)
+
+
 def boundary_mask_nodes(n: int):
     i = np.arange(n + 1)
     I, J = np.meshgrid(i, i, indexing="xy")

@@ -681,6 +681,333 @@ __global__ void __launch_bounds__(kTThreads, 2) k_assemble_tiled(Phys ph, int Nn
   if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = bs;
 }
 
+// ------------------------------------------------------------------ K1, modal element algebra
+// Same tiling as k_assemble_tiled, with the per-cell algebra reorganised around the structure
+// of the uniform Q1 cell (exact identities, not approximations):
+//  * dN_a/dx(q) = (xi_a + xe_a eta_q)/(2dx), dN_a/dy(q) = (eta_a + xe_a xi_q)/(2dx) with
+//    xe_a = xi_a eta_a, so tau^(N_a e_k)(q) = W_{q,k} mode_a/(2dx), mode_a = (xi_a, eta_a, xe_a),
+//    and every column of W lies in span{p1, p2, p3}:
+//      p1 = (al, be, 0), p2 = (0, 0, be), p3 = (al, -be, 0)   (al = 1/sqrt2, be = 1/(sqrt2 e)).
+//    The element stiffness sum_q w dt tau^_a . C_q tau^_b (eq:linearSVNewton + eq:modification)
+//    is therefore mode_a^T S mode_b with a 6x6 S (15 distinct entries) accumulated from the six
+//    Q_ij = p_i^T C_q p_j = c0 p_i.p_j - c1 (a_i b_j + a_j b_i), a_i = p_i.pi^, b_i = p_i.tau^.
+//  * N_a(q) = phi_a . m_q / 4 with phi_a = (1, xi_a, eta_a, xe_a), m_q = (1, xi_q, eta_q, xi_q eta_q),
+//    so the mass + ocean-drag block sum_q w N_a N_b E_km(q) needs only the four moments
+//    (1, xi_q, eta_q, xi_q eta_q) of E_km:
+//      phi_a^T M phi_b / 16 = [mu0 (1+g2 X_aX_b)(1+g2 Y_aY_b) + mux (X_a+X_b)(1+g2 Y_aY_b)
+//                              + muy (Y_a+Y_b)(1+g2 X_aX_b) + muxy (X_a+X_b)(Y_a+Y_b)] / 16.
+// This cuts the fp64 work per cell ~3x (the tiled kernel is fp64-pipe bound, ncu r01).
+__host__ __device__ constexpr int lidx(int x, int y) { return y ? (x ? 2 : 3) : (x ? 1 : 0); }
+__host__ __device__ constexpr double xe_a(int a) { return xi_a(a) * eta_a(a); }
+__host__ __device__ constexpr double mode_c(int a, int c) { return c == 0 ? xi_a(a) : c == 1 ? eta_a(a) : xe_a(a); }
+
+// Per-step constants of the modal element algebra, computed on the host so the kernel reads
+// them as constant-bank operands (no registers, no device divisions).
+struct ElemK {
+  double al, be, al2, be2, sc, pp11, pp13, pp22, w, wdt, co, dtco, dmin2, prf, hb;
+};
+static ElemK make_elemk(const Phys& ph) {
+  ElemK k;
+  const double inv_dx = 1.0 / ph.dx;
+  k.al = kR2I;
+  k.be = kR2I / ph.e;
+  k.al2 = 2.0 * inv_dx * k.al;
+  k.be2 = 2.0 * inv_dx * k.be;
+  k.w = 0.25 * ph.dx * ph.dx;
+  k.wdt = k.w * ph.dt;
+  k.sc = k.wdt * 0.25 * inv_dx * inv_dx;
+  k.pp11 = k.al * k.al + k.be * k.be;
+  k.pp13 = k.al * k.al - k.be * k.be;
+  k.pp22 = k.be * k.be;
+  k.co = ph.C_o * ph.rho_o;
+  k.dtco = ph.dt * k.co;
+  k.dmin2 = ph.delta_min * ph.delta_min;
+  k.prf = k.wdt * inv_dx;
+  k.hb = 0.5 * k.wdt * inv_dx;
+  return k;
+}
+
+template <int KIND>
+__device__ __forceinline__ void element_modal(const Phys& ph, const ElemK& K, int ci, int cj, const double* __restrict__ v,
+                                              const double* __restrict__ vo, const double* __restrict__ pi,
+                                              const double* __restrict__ P, const double* __restrict__ rhoh,
+                                              double* __restrict__ Ks, double* __restrict__ Rs, int t) {
+  const int n = ph.n, s = n + 1;
+  const long long Nc = (long long)n * n;
+  const int cell = cj * n + ci;
+  // Modal coefficients of the nodal fields: u(xi, eta) = m0 + m1 xi + m2 eta + m3 xi eta
+  // (nodes CCW from (-1,-1)); grad u = (2/dx) (m1 + m3 eta, m2 + m3 xi).
+  double mu[4][2], mw[4][2];  // velocity v and ocean-relative velocity v_o - v
+  {
+    const int nd0 = cj * s + ci;
+    const int ids[4] = {nd0, nd0 + 1, nd0 + s + 1, nd0 + s};
+    double u[4][2], dw[4][2];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const double2 a1 = __ldg(reinterpret_cast<const double2*>(v) + ids[b]);
+      const double2 a2 = __ldg(reinterpret_cast<const double2*>(vo) + ids[b]);
+      u[b][0] = a1.x; u[b][1] = a1.y;
+      dw[b][0] = a2.x - a1.x; dw[b][1] = a2.y - a1.y;
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      mu[0][c] = 0.25 * ((u[0][c] + u[2][c]) + (u[1][c] + u[3][c]));
+      mu[1][c] = 0.25 * ((u[1][c] + u[2][c]) - (u[0][c] + u[3][c]));
+      mu[2][c] = 0.25 * ((u[2][c] + u[3][c]) - (u[0][c] + u[1][c]));
+      mu[3][c] = 0.25 * ((u[0][c] + u[2][c]) - (u[1][c] + u[3][c]));
+      mw[0][c] = 0.25 * ((dw[0][c] + dw[2][c]) + (dw[1][c] + dw[3][c]));
+      mw[1][c] = 0.25 * ((dw[1][c] + dw[2][c]) - (dw[0][c] + dw[3][c]));
+      mw[2][c] = 0.25 * ((dw[2][c] + dw[3][c]) - (dw[0][c] + dw[1][c]));
+      mw[3][c] = 0.25 * ((dw[0][c] + dw[2][c]) - (dw[1][c] + dw[3][c]));
+    }
+  }
+  const double Pc = P[cell], rh = rhoh[cell];
+  const double w = K.w, wdt = K.wdt, al = K.al, be = K.be, al2 = K.al2, be2 = K.be2;  // al2 = (2/dx) al
+  const double co = K.co, dmin2 = K.dmin2, sc = K.sc;                                 // sc = w dt/(2dx)^2
+  const double pp11 = K.pp11, pp13 = K.pp13, pp22 = K.pp22;
+  constexpr double g2 = 1.0 / 3.0;
+  // The per-Gauss-point Q_ij and drag coefficients are parked in this thread's 36 Ks slots
+  // (slot 9q + j) and combined after the loop: that keeps the loop's live state small.
+  // Residual moments: F_k = sum_q f_k (1, xi, eta, xi eta), B = sums of c0 b_i (see below).
+  double fx0 = 0, fx1 = 0, fx2 = 0, fx3 = 0, fy0 = 0, fy1 = 0, fy2 = 0, fy3 = 0;
+  double B1 = 0, B2 = 0, B3 = 0, B4 = 0, B5 = 0;
+  // pi of the next Gauss point is fetched one iteration ahead (software pipelining)
+  double pn0 = 0.0, pn1 = 0.0, pn2 = 0.0;
+  if (KIND == SEAICE_JAC_SV) {
+    pn0 = __ldg(pi + cell); pn1 = __ldg(pi + 4 * Nc + cell); pn2 = __ldg(pi + 8 * Nc + cell);
+  }
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) {
+    const double xq = xi_q(q), eq = eta_q(q), xe = xq * eq;
+    const double p11 = pn0, p12 = pn1, p22 = pn2;
+    if (KIND == SEAICE_JAC_SV && q < 3) {
+      pn0 = __ldg(pi + (q + 1) * Nc + cell); pn1 = __ldg(pi + (5 + q) * Nc + cell); pn2 = __ldg(pi + (9 + q) * Nc + cell);
+    }
+    const double vx = mu[0][0] + mu[1][0] * xq + mu[2][0] * eq + mu[3][0] * xe;
+    const double vy = mu[0][1] + mu[1][1] * xq + mu[2][1] * eq + mu[3][1] * xe;
+    const double wx = mw[0][0] + mw[1][0] * xq + mw[2][0] * eq + mw[3][0] * xe;
+    const double wy = mw[0][1] + mw[1][1] * xq + mw[2][1] * eq + mw[3][1] * xe;
+    // reference-scaled gradient (physical = 2/dx times this)
+    const double L00 = mu[1][0] + mu[3][0] * eq, L01 = mu[2][0] + mu[3][0] * xq;
+    const double L10 = mu[1][1] + mu[3][1] * eq, L11 = mu[2][1] + mu[3][1] * xq;
+    const double tx = al2 * (L00 + L11), ty = be2 * (L00 - L11), tz = be2 * (L01 + L10);  // tau^(v)
+    const double X = dmin2 + 2.0 * (tx * tx + ty * ty + tz * tz);  // Delta^2 >= Delta_min^2 > 0
+    const double rD = rsqrt(X);                                      // 1/Delta
+    const double c0 = Pc * rD;
+    const double b1 = al * tx + be * ty, b2 = be * tz, b3 = al * tx - be * ty;
+    const double cs = sc * c0;
+    double Q11 = cs * pp11, Q13 = cs * pp13, Q22 = cs * pp22, Q33 = cs * pp11, Q12 = 0.0, Q23 = 0.0;
+    if (KIND == SEAICE_JAC_SV) {
+      const V3 ph_ = pi_hat(p11, p12, p22);
+      const double a1 = al * ph_.x + be * ph_.y, a2 = be * ph_.z, a3 = al * ph_.x - be * ph_.y;
+      // 1/s = 1/max(1, sqrt2 |pi^|)
+      const double pq = 2.0 * dot3(ph_, ph_);
+      const double isf = pq > 1.0 ? rsqrt(pq) : 1.0;
+      const double c1 = sc * Pc * (rD * rD) * isf;
+      Q11 -= c1 * 2.0 * a1 * b1;
+      Q12 = -c1 * (a1 * b2 + a2 * b1);
+      Q13 -= c1 * (a1 * b3 + a3 * b1);
+      Q22 -= c1 * 2.0 * a2 * b2;
+      Q23 = -c1 * (a2 * b3 + a3 * b2);
+      Q33 -= c1 * 2.0 * a3 * b3;
+    } else if (KIND == SEAICE_JAC_STD) {
+      const double c1 = sc * 2.0 * Pc * (rD * rD * rD);
+      Q11 -= c1 * b1 * b1;
+      Q12 = -c1 * b1 * b2;
+      Q13 -= c1 * b1 * b3;
+      Q22 -= c1 * b2 * b2;
+      Q23 = -c1 * b2 * b3;
+      Q33 -= c1 * b3 * b3;
+    }
+    double* slot = Ks + (9 * q) * kTC + t;
+    slot[0 * kTC] = Q11; slot[1 * kTC] = Q12; slot[2 * kTC] = Q13;
+    slot[3 * kTC] = Q22; slot[4 * kTC] = Q23; slot[5 * kTC] = Q33;
+    // ocean drag linearisation D = C_o rho_o (|w| I + w w^T/|w|), w = v_o - v (eq:A)
+    const double n2 = wx * wx + wy * wy;
+    double nw, inw = 0.0;
+    if (n2 >= 1e-24) {  // |w| >= 1e-12
+      const double r = rsqrt(n2);
+      nw = n2 * r;
+      inw = co * r;
+    } else {
+      nw = sqrt(n2);
+    }
+    const double d00 = co * nw + inw * wx * wx, d11 = co * nw + inw * wy * wy, d01 = inw * wx * wy;
+    slot[6 * kTC] = wdt * d00; slot[7 * kTC] = wdt * d11; slot[8 * kTC] = wdt * d01;
+    // residual moments (mass + drag part f_k, stress part c0 b_i)
+    const double fx = w * (rh * vx - K.dtco * nw * wx), fy = w * (rh * vy - K.dtco * nw * wy);
+    fx0 += fx; fx1 += xq * fx; fx2 += eq * fx; fx3 += xe * fx;
+    fy0 += fy; fy1 += xq * fy; fy2 += eq * fy; fy3 += xe * fy;
+    const double e1 = c0 * b1, e2 = c0 * b2, e3 = c0 * b3;
+    B1 += e1; B2 += e2; B3 += e3;
+    B4 += eq * e1 + xq * e2;
+    B5 += xq * e3 + eq * e2;
+  }
+  // element residual -A(v, phi_{a,k}):
+  //   -sum_q N_a f_k = -(F0 + X F1 + Y F2 + XY F3)/4,
+  //   -sum_q w dt c0 tau^(v).tau^(N_a e_k) = -(w dt/(2dx)) (X B1 + Y B2 + XY B4)  (k = x)
+  //                                          -(w dt/(2dx)) (Y B3 + X B2 + XY B5)  (k = y),
+  //   + w dt (P/2) sum_q dN_a/dx_k = w dt P X/dx (resp. Y).
+  const double pr = K.prf * Pc, hb = K.hb;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const double X = xi_a(a), Y = eta_a(a), XY = xe_a(a);
+    const double rx = -(0.25 * (fx0 + X * fx1 + Y * fx2 + XY * fx3) + hb * (X * B1 + Y * B2 + XY * B4)) + pr * X;
+    const double ry = -(0.25 * (fy0 + X * fy1 + Y * fy2 + XY * fy3) + hb * (Y * B3 + X * B2 + XY * B5)) + pr * Y;
+    Rs[(2 * a) * kTC + t] = rx;
+    Rs[(2 * a + 1) * kTC + t] = ry;
+  }
+  // accumulate S (15 distinct entries) and the drag moments from the parked values
+  double s00 = 0, s01 = 0, s02 = 0, s11 = 0, s12 = 0, s22 = 0, s04 = 0, s05 = 0, s14 = 0, s15 = 0, s24 = 0,
+         s25 = 0, s44 = 0, s45 = 0, s55 = 0;
+  double mx0 = 0, mx1 = 0, mx2 = 0, mx3 = 0, my0 = 0, my1 = 0, my2 = 0, my3 = 0, mc0 = 0, mc1 = 0, mc2 = 0, mc3 = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    constexpr double g2c = 1.0 / 3.0;
+    const double xq = xi_q(q), eq = eta_q(q), xe = xq * eq;
+    const double* slot = Ks + (9 * q) * kTC + t;
+    const double Q11 = slot[0], Q12 = slot[1 * kTC], Q13 = slot[2 * kTC], Q22 = slot[3 * kTC],
+                 Q23 = slot[4 * kTC], Q33 = slot[5 * kTC];
+    s00 += Q11; s01 += Q12; s02 += eq * Q11 + xq * Q12;
+    s11 += Q22; s12 += eq * Q12 + xq * Q22; s22 += g2c * (Q11 + Q22) + 2.0 * xe * Q12;
+    s04 += Q13; s05 += eq * Q12 + xq * Q13; s14 += Q23; s15 += eq * Q22 + xq * Q23;
+    s24 += eq * Q13 + xq * Q23; s25 += g2c * (Q12 + Q23) + xe * (Q13 + Q22);
+    s44 += Q33; s45 += eq * Q23 + xq * Q33; s55 += g2c * (Q22 + Q33) + 2.0 * xe * Q23;
+    const double d00 = slot[6 * kTC], d11 = slot[7 * kTC], d01 = slot[8 * kTC];
+    mx0 += d00; mx1 += xq * d00; mx2 += eq * d00; mx3 += xe * d00;
+    my0 += d11; my1 += xq * d11; my2 += eq * d11; my3 += xe * d11;
+    mc0 += d01; mc1 += xq * d01; mc2 += eq * d01; mc3 += xe * d01;
+  }
+  // consistent mass: E_kk += w rh at every Gauss point -> mu0 += 4 w rh
+  mx0 += 4.0 * w * rh;
+  my0 += 4.0 * w * rh;
+  // S blocks (rows/cols 0..2 = x modes, 3..5 = y modes)
+  const double S[6][6] = {{s00, s01, s02, s01, s04, s05}, {s01, s11, s12, s11, s14, s15},
+                          {s02, s12, s22, s12, s24, s25}, {s01, s11, s12, s11, s14, s15},
+                          {s04, s14, s24, s14, s44, s45}, {s05, s15, s25, s15, s45, s55}};
+#pragma unroll
+  for (int qq = 0; qq < 8; ++qq) {
+    const int b = qq >> 1, m = qq & 1;
+    double h[6];
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc = (mode_c(b, c) > 0) ? acc + S[r][3 * m + c] : acc - S[r][3 * m + c];
+      h[r] = acc;
+    }
+#pragma unroll
+    for (int pp = 0; pp <= qq; ++pp) {
+      const int a = pp >> 1, k = pp & 1;
+      double val = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) val = (mode_c(a, c) > 0) ? val + h[3 * k + c] : val - h[3 * k + c];
+      const bool xx = (k == 0 && m == 0), yy = (k == 1 && m == 1);
+      const double mu0 = xx ? mx0 : yy ? my0 : mc0, mu1 = xx ? mx1 : yy ? my1 : mc1;
+      const double mu2 = xx ? mx2 : yy ? my2 : mc2, mu3 = xx ? mx3 : yy ? my3 : mc3;
+      const double XX = xi_a(a) * xi_a(b), YY = eta_a(a) * eta_a(b);
+      const double sx = xi_a(a) + xi_a(b), sy = eta_a(a) + eta_a(b);
+      double md = mu0 * ((1.0 + g2 * XX) * (1.0 + g2 * YY));
+      if (sx != 0.0) md += mu1 * (sx * (1.0 + g2 * YY));
+      if (sy != 0.0) md += mu2 * (sy * (1.0 + g2 * XX));
+      if (sx != 0.0 && sy != 0.0) md += mu3 * (sx * sy);
+      Ks[ke_idx(pp, qq) * kTC + t] = val + 0.0625 * md;
+    }
+  }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kTThreads, 2) k_assemble_modal(Phys ph, ElemK K, int Nn, const double* __restrict__ v,
+                                                                 const double* __restrict__ pi,
+                                                                 const double* __restrict__ P,
+                                                                 const double* __restrict__ rhoh,
+                                                                 const double* __restrict__ vo,
+                                                                 const double* __restrict__ F,
+                                                                 double* __restrict__ Jst, double* __restrict__ R,
+                                                                 double* __restrict__ part) {
+  extern __shared__ double smem[];
+  double* Ks = smem;             // [36][kTC]
+  double* Rs = smem + kKE * kTC;  // [8][kTC]
+  __shared__ double sh[32];
+  const int n = ph.n, s = n + 1;
+  const int i0 = blockIdx.x * kTX, j0 = blockIdx.y * kTY;
+  const int t = threadIdx.x;
+  {
+    const int ci = i0 - 1 + t % (kTX + 1), cj = j0 - 1 + t / (kTX + 1);
+    if (ci >= 0 && ci < n && cj >= 0 && cj < n) element_modal<KIND>(ph, K, ci, cj, v, vo, pi, P, rhoh, Ks, Rs, t);
+  }
+  __syncthreads();
+  double nrm = 0.0;
+  if (t < kTX * kTY) {
+    const int i = i0 + t % kTX, j = j0 + t / kTX;
+    if (i <= n && j <= n) {
+      const int node = j * s + i;
+      if (!(i > 0 && i < n && j > 0 && j < n)) {
+#pragma unroll
+        for (int e = 0; e < 36; ++e) Jst[(long long)e * Nn + node] = (e == 16 || e == 19) ? 1.0 : 0.0;
+        R[2 * node] = 0.0;
+        R[2 * node + 1] = 0.0;
+      } else {
+        // cell cc at offset (cc&1, cc>>1) from (i-1, j-1); the node is its local corner (1-ox, 1-oy)
+        const int lc0 = (i - i0) + (j - j0) * (kTX + 1);
+        double r0 = F[2 * node], r1 = F[2 * node + 1];
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int a = lidx(1 - (cc & 1), 1 - (cc >> 1));
+          const int lc = lc0 + (cc & 1) + (cc >> 1) * (kTX + 1);
+          r0 += Rs[(2 * a) * kTC + lc];
+          r1 += Rs[(2 * a + 1) * kTC + lc];
+        }
+        R[2 * node] = r0;
+        R[2 * node + 1] = r1;
+        nrm = r0 * r0 + r1 * r1;
+#pragma unroll
+        for (int sl = 0; sl < 9; ++sl) {
+          const int dxs = sl % 3 - 1, dys = sl / 3 - 1;
+          const bool bnd = (i + dxs == 0 || i + dxs == n || j + dys == 0 || j + dys == n);  // symmetric elimination
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int k = e >> 1, m = e & 1;
+            double acc = 0.0;
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+              const int ax = 1 - (cc & 1), ay = 1 - (cc >> 1);
+              const int bx = ax + dxs, by = ay + dys;
+              if (bx < 0 || bx > 1 || by < 0 || by > 1) continue;
+              const int p = 2 * lidx(ax, ay) + k, q = 2 * lidx(bx, by) + m;
+              const int lc = lc0 + (cc & 1) + (cc >> 1) * (kTX + 1);
+              acc += Ks[(p <= q ? ke_idx(p, q) : ke_idx(q, p)) * kTC + lc];
+            }
+            Jst[(long long)(sl * 4 + e) * Nn + node] = bnd ? 0.0 : acc;
+          }
+        }
+      }
+    }
+  }
+  const double bs = block_sum(nrm, sh);
+  if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = bs;
+}
+
+template <int KIND>
+static int launch_assemble_modal(Ctx& c, const double* v, const double* pi, double* R) {
+  static bool attr = false;
+  if (!attr) {
+    SI_CUDA(cudaFuncSetAttribute(k_assemble_modal<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kTileSmem));
+    attr = true;
+  }
+  const dim3 grid((c.n + 1 + kTX - 1) / kTX, (c.n + 1 + kTY - 1) / kTY);
+  const int g = grid.x * grid.y;
+  c.part.ensure(c.al, g + 64);
+  prof_begin(c);
+  k_assemble_modal<KIND><<<grid, kTThreads, kTileSmem, c.s>>>(c.ph, make_elemk(c.ph), c.Nn, v, pi, c.P.get(), c.rhoh.get(),
+                                                               c.vocean.get(), c.F.get(), c.Jst.get(), R,
+                                                               c.part.get());
+  SI_LAUNCHED(c);
+  prof_end(c, PC_ASSEMBLE, 352.0 * c.Nn + 112.0 * c.Nc);
+  return g;
+}
+
 template <int KIND>
 static int launch_assemble_tiled(Ctx& c, const double* v, const double* pi, double* R) {
   static bool attr = false;
@@ -721,12 +1048,16 @@ void assemble_impl(Ctx& c, const double* v, const double* pi, bool jac, double* 
   int nparts = grid_for(c.Nn, 128);
   if (!jac) {
     launch_assemble<SEAICE_JAC_PICARD, false>(c, v, pp, R);  // residual only: per-node gather
+  } else if (getenv("SEAICE_ASM_OLD")) {
+    if (kind == SEAICE_JAC_SV) nparts = launch_assemble_tiled<SEAICE_JAC_SV>(c, v, pp, R);
+    else if (kind == SEAICE_JAC_STD) nparts = launch_assemble_tiled<SEAICE_JAC_STD>(c, v, pp, R);
+    else nparts = launch_assemble_tiled<SEAICE_JAC_PICARD>(c, v, pp, R);
   } else if (kind == SEAICE_JAC_SV) {
-    nparts = launch_assemble_tiled<SEAICE_JAC_SV>(c, v, pp, R);
+    nparts = launch_assemble_modal<SEAICE_JAC_SV>(c, v, pp, R);
   } else if (kind == SEAICE_JAC_STD) {
-    nparts = launch_assemble_tiled<SEAICE_JAC_STD>(c, v, pp, R);
+    nparts = launch_assemble_modal<SEAICE_JAC_STD>(c, v, pp, R);
   } else {
-    nparts = launch_assemble_tiled<SEAICE_JAC_PICARD>(c, v, pp, R);
+    nparts = launch_assemble_modal<SEAICE_JAC_PICARD>(c, v, pp, R);
   }
   if (r_out) {
     SI_CUDA(cudaMemcpyAsync(r_out, R, sizeof(double) * c.N, cudaMemcpyDeviceToDevice, c.s));

@@ -1296,9 +1296,37 @@ __global__ void k_bsr_spmv_add(int nb, const int* __restrict__ rp, const int* __
 }
 
 // ------------------------------------------------------------------ group-per-row BSR kernels
+// V-cycle copy of a block array in the chunk-of-32 SoA layout (Level::valT): a group's lanes
+// read consecutive blocks, so each per-element load of the warp is contiguous.
+__global__ void k_tile_blocks(long long nnzb, int BB, const double* __restrict__ val, double* __restrict__ out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= nnzb * BB) return;
+  const long long e = i / BB;
+  const int j = (int)(i - e * BB);
+  out[((e >> 5) * BB + j) * 32 + (e & 31)] = val[i];
+}
+static void tile_copy(Ctx& c, DBuf<double>& out, const double* val, long long nnzb, int BB) {
+  const long long n = (nnzb + 31) / 32 * 32 * BB;
+  out.ensure(c.al, (size_t)(n > 0 ? n : 1));
+  if (nnzb == 0) return;
+  k_tile_blocks<<<grid_for(nnzb * BB), kThreads, 0, c.s>>>(nnzb, BB, val, out.get());
+  SI_LAUNCHED(c);
+}
+
 // G consecutive lanes own one block row: lane l reads blocks e = rp[row] + l, + G, ...
 // so the G blocks a group touches per step are contiguous in memory (coalesced), and the
-// BR partial sums are combined with an xor-butterfly (same order on every lane).
+// BR partial sums are combined with an xor-butterfly (same order on every lane).  The loop is
+// unrolled by two so both column-index loads (and then both x gathers) are in flight together.
+template <int BR, int BC>
+__device__ __forceinline__ void blk_fma(const double* __restrict__ val, int e, const double xv[BC], double acc[BR]) {
+  const double* v = val + (long long)(e >> 5) * (BR * BC * 32) + (e & 31);  // chunk-of-32 SoA
+#pragma unroll
+  for (int a = 0; a < BR; ++a)
+#pragma unroll
+    for (int b = 0; b < BC; ++b) acc[a] += __ldg(v + (a * BC + b) * 32) * xv[b];
+}
+
+constexpr bool kUnroll2 = true;
 template <int BR, int BC, int G>
 __device__ __forceinline__ void grp_row(int row, int nb, int lig, const int* __restrict__ rp,
                                         const int* __restrict__ ci, const double* __restrict__ val,
@@ -1307,16 +1335,24 @@ __device__ __forceinline__ void grp_row(int row, int nb, int lig, const int* __r
   for (int a = 0; a < BR; ++a) acc[a] = 0.0;
   if (row < nb) {
     const int e1 = __ldg(rp + row + 1);
-    for (int e = __ldg(rp + row) + lig; e < e1; e += G) {
-      const int col = __ldg(ci + e);
-      double xv[BC];
+    int e = __ldg(rp + row) + lig;
+    for (; kUnroll2 && e + G < e1; e += 2 * G) {
+      const int c0 = __ldg(ci + e), c1 = __ldg(ci + e + G);
+      double x0[BC], x1[BC];
 #pragma unroll
-      for (int b = 0; b < BC; ++b) xv[b] = __ldg(x + (long long)col * BC + b);
-      const double* v = val + (long long)e * BR * BC;
+      for (int b = 0; b < BC; ++b) {
+        x0[b] = __ldg(x + (long long)c0 * BC + b);
+        x1[b] = __ldg(x + (long long)c1 * BC + b);
+      }
+      blk_fma<BR, BC>(val, e, x0, acc);
+      blk_fma<BR, BC>(val, e + G, x1, acc);
+    }
+    for (; e < e1; e += G) {
+      const int c0 = __ldg(ci + e);
+      double x0[BC];
 #pragma unroll
-      for (int a = 0; a < BR; ++a)
-#pragma unroll
-        for (int b = 0; b < BC; ++b) acc[a] += __ldcs(v + a * BC + b) * xv[b];
+      for (int b = 0; b < BC; ++b) x0[b] = __ldg(x + (long long)c0 * BC + b);
+      blk_fma<BR, BC>(val, e, x0, acc);
     }
   }
 #pragma unroll
@@ -1325,6 +1361,19 @@ __device__ __forceinline__ void grp_row(int row, int nb, int lig, const int* __r
     for (int a = 0; a < BR; ++a) acc[a] += __shfl_xor_sync(0xffffffffu, acc[a], off, G);
 }
 
+// component `a` of a register array without dynamic indexing
+template <int B>
+__device__ __forceinline__ double pick(const double v[B], int a) {
+  double r = v[0];
+#pragma unroll
+  for (int k = 1; k < B; ++k) r = (a == k) ? v[k] : r;
+  return r;
+}
+
+// The row epilogues are spread over the group: lane a < B owns component a of the block row
+// (its loads are issued before the SpMV loop), and the B x B block-Jacobi product gathers the
+// other components of r with shuffles inside the group.
+
 // y = A x (add = 0) or y += A x (add = 1)
 template <int BR, int BC, int G>
 __global__ void __launch_bounds__(256) k_gspmv(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
@@ -1332,15 +1381,12 @@ __global__ void __launch_bounds__(256) k_gspmv(int nb, const int* __restrict__ r
                                                double* __restrict__ y, int add) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int row = (int)(t / G), lig = (int)(t % G);
+  const bool own = row < nb && lig < BR;
+  const long long i = (long long)row * BR + lig;
+  const double y0 = (own && add) ? y[i] : 0.0;
   double acc[BR];
   grp_row<BR, BC, G>(row, nb, lig, rp, ci, val, x, acc);
-  if (row < nb && lig == 0) {
-#pragma unroll
-    for (int a = 0; a < BR; ++a) {
-      const long long i = (long long)row * BR + a;
-      y[i] = add ? y[i] + acc[a] : acc[a];
-    }
-  }
+  if (own) y[i] = y0 + pick<BR>(acc, lig);
 }
 
 // fused Chebyshev step (same semantics as k_cheb_stencil) on a coarse level
@@ -1390,28 +1436,28 @@ __global__ void __launch_bounds__(256) k_gresid(int nb, const int* __restrict__ 
                                                 double* __restrict__ r, double* __restrict__ d, double c2) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int row = (int)(t / G), lig = (int)(t % G);
+  const bool own = row < nb && lig < B;
+  const long long i = (long long)row * B + lig;
+  double bo = 0.0, D[B];
+#pragma unroll
+  for (int k = 0; k < B; ++k) D[k] = 0.0;
+  if (own) {
+    bo = b[i];
+#pragma unroll
+    for (int k = 0; k < B; ++k) D[k] = __ldg(dinv + (long long)row * B * B + lig * B + k);
+  }
   double acc[B];
   if (x) grp_row<B, B, G>(row, nb, lig, rp, ci, val, x, acc);
   else {
 #pragma unroll
     for (int a = 0; a < B; ++a) acc[a] = 0.0;
   }
-  if (row >= nb || lig != 0) return;
-  double rv[B];
+  const double rv = bo - (own ? pick<B>(acc, lig) : 0.0);
+  if (own) r[i] = rv;
+  double z = 0.0;
 #pragma unroll
-  for (int a = 0; a < B; ++a) {
-    const long long i = (long long)row * B + a;
-    rv[a] = b[i] - acc[a];
-    r[i] = rv[a];
-  }
-  const double* D = dinv + (long long)row * B * B;
-#pragma unroll
-  for (int a = 0; a < B; ++a) {
-    double z = 0.0;
-#pragma unroll
-    for (int bb = 0; bb < B; ++bb) z += D[a * B + bb] * rv[bb];
-    d[(long long)row * B + a] = c2 * z;
-  }
+  for (int k = 0; k < B; ++k) z += D[k] * __shfl_sync(0xffffffffu, rv, k, G);
+  if (own) d[i] = c2 * z;
 }
 
 static int pick_group(long long nnzb, int nb) {
@@ -1472,7 +1518,7 @@ static double power_lambda(Ctx& c, Level& L, int lvl) {
     if (lvl == 0 && B == 2)
       stencil_spmv(c, x, y);  // the finest operator is the stencil itself
     else
-      gspmv(c, L.nb, B, B, L.nnzb, L.rp.get(), L.ci.get(), L.val.get(), x, y, 0);
+      gspmv(c, L.nb, B, B, L.nnzb, L.rp.get(), L.ci.get(), L.valT.get(), x, y, 0);
     k_dinv_apply<B><<<grid_for(L.nb), kThreads, 0, c.s>>>(L.nb, L.dinv.get(), y);
     k_sqnorm_part<<<g, kThreads, 0, c.s>>>(N, y, part);
     k_sum_to<<<1, 1024, 0, c.s>>>(part, g, ny2);
@@ -1710,6 +1756,7 @@ void amg_setup_impl(Ctx& c) {
     if (L.b == 2) level_diag<2>(c, L, S, dnorm);
     else level_diag<3>(c, L, S, dnorm);
     tick(c, "diag", lvl);
+    if (lvl > 0) tile_copy(c, L.valT, L.val.get(), L.nnzb, L.b * L.b);
     L.lmax = (L.b == 2) ? power_lambda<2>(c, L, lvl) : power_lambda<3>(c, L, lvl);
     tick(c, "power", lvl);
     nnz_total += L.nnzb * L.b * L.b;
@@ -1727,6 +1774,8 @@ void amg_setup_impl(Ctx& c) {
     ++c.nlev;
     if (Lf.b == 2) build_transfer<2>(c, Lf, Lc, lvl, na, S);
     else build_transfer<3>(c, Lf, Lc, lvl, na, S);
+    tile_copy(c, Lf.PvalT, Lf.Pval.get(), Lf.Pnnzb, Lf.b * 3);
+    tile_copy(c, Lf.RvalT, Lf.Rval.get(), Lf.Rnnzb, 3 * Lf.b);
   }
   Level& Lc = c.lv[c.nlev - 1];
   const long long nd = (long long)Lc.nb * Lc.b;
@@ -1773,7 +1822,7 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
   } else {
     const int G = pick_group(L.nnzb, L.nb);
     SI_GDISPATCH(G, (k_gresid<3, GG><<<ggrid(L.nb, GG), 256, 0, c.s>>>(
-                        L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), b, pre ? nullptr : x, r, d,
+                        L.nb, L.rp.get(), L.ci.get(), L.valT.get(), L.dinv.get(), b, pre ? nullptr : x, r, d,
                         1.0 / k.th)))
   }
   SI_LAUNCHED(c);
@@ -1797,7 +1846,7 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
                                                      want_d);
     } else {
       const int G = pick_group(L.nnzb, L.nb);
-      SI_GDISPATCH(G, (k_gcheb<3, GG><<<ggrid(L.nb, GG), 256, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.val.get(),
+      SI_GDISPATCH(G, (k_gcheb<3, GG><<<ggrid(L.nb, GG), 256, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.valT.get(),
                                                                        L.dinv.get(), d, r, x, d2, c1, c2, first,
                                                                        want_r, want_d)))
     }
@@ -1827,12 +1876,12 @@ static void vcycle_level(Ctx& c, int l, const double* b, double* x) {
   Level& Lc = c.lv[l + 1];
   // r_c = R r
   prof_begin(c);
-  gspmv(c, L.nbc, 3, L.b, L.Rnnzb, L.Rrp.get(), L.Rci.get(), L.Rval.get(), L.r.get(), Lc.rhs.get(), 0);
+  gspmv(c, L.nbc, 3, L.b, L.Rnnzb, L.Rrp.get(), L.Rci.get(), L.RvalT.get(), L.r.get(), Lc.rhs.get(), 0);
   prof_end(c, PC_TRANSFER, L.Rnnzb * (24.0 * L.b + 4.0) + 4.0 * (L.nbc + 1) + 8.0 * L.b * L.nb + 24.0 * L.nbc);
   vcycle_level(c, l + 1, Lc.rhs.get(), Lc.x.get());
   // x += P e_c
   prof_begin(c);
-  gspmv(c, L.nb, L.b, 3, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.Pval.get(), Lc.x.get(), x, 1);
+  gspmv(c, L.nb, L.b, 3, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.PvalT.get(), Lc.x.get(), x, 1);
   prof_end(c, PC_TRANSFER, L.Pnnzb * (24.0 * L.b + 4.0) + 4.0 * (L.nb + 1) + 16.0 * L.b * L.nb + 24.0 * L.nbc);
   smooth(c, l, b, x, false);
 }

@@ -28,6 +28,9 @@ struct Level {
   // V-cycle work vectors (length nb*b)
   DBuf<double> x, rhs, r, d, d2, z;
   DBuf<double> Tval;          // A P_tent values (pattern of P), setup scratch kept for reuse
+  // V-cycle copies of val / Pval / Rval in the chunk-of-32 SoA layout read by the group-per-row
+  // kernels: element j of block e at ((e >> 5) * BB + j) * 32 + (e & 31)  (coalesced loads)
+  DBuf<double> valT, PvalT, RvalT;
 };
 
 // Grow-only chunked bump allocator for setup scratch (LIFO marks): avoids an allocator

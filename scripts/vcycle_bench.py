@@ -20,6 +20,7 @@ ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--iterate", type=int, default=8)
 ap.add_argument("--reps", type=int, default=50)
 ap.add_argument("--params", default="{}")
+ap.add_argument("--ncu-range", action="store_true", help="wrap one V-cycle in cudaProfilerStart/Stop")
 a = ap.parse_args()
 cfg = wl.CONFIGS[a.config]
 h, A = wl.ice_fields(cfg)
@@ -61,6 +62,12 @@ for k, d in p.items():
     if d["launches"]:
         print(f"  {k:14s} {d['ms']/5*1e3:9.1f} us/vcycle  {d['launches']/5:5.1f} launches  "
               f"{d['bytes']/max(d['ms'],1e-9)/1e6:8.1f} GB/s")
+if a.ncu_range:
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    ctx.precond_apply(r)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
 R, _ = ctx.residual(v)
 x, st, rc = ctx.fgmres(R)
 torch.cuda.synchronize()

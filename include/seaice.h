@@ -82,6 +82,8 @@ typedef struct {
   uint64_t amg_seed;
   int32_t agg_dist0;       /* aggregation root distance on the finest level: 2 = MIS(2) (default), 1 = MIS(1) */
   int32_t agg_dist;        /* same on coarse levels */
+  int32_t cheb_fused;      /* 1 (default): finest-level Chebyshev(3) as one temporally blocked launch
+                              (same arithmetic per node and step); 0: one launch per step */
 } seaice_params;
 
 /* Compressed-sparse-row view (scalar rows). Index arrays int32, values fp64. */

@@ -64,6 +64,7 @@ void validate(const seaice_params* p) {
   SI_CHECK(p->coarse_max_dof >= 3 && p->coarse_max_dof <= 8192, SEAICE_EINVAL, "coarse_max_dof in [3,8192]");
   SI_CHECK((p->agg_dist0 == 1 || p->agg_dist0 == 2) && (p->agg_dist == 1 || p->agg_dist == 2), SEAICE_EINVAL,
            "agg_dist0/agg_dist must be 1 or 2");
+  SI_CHECK(p->cheb_fused == 0 || p->cheb_fused == 1, SEAICE_EINVAL, "cheb_fused must be 0 or 1");
 }
 
 int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* out) {
@@ -225,6 +226,7 @@ void seaice_default_params(seaice_params* p, int32_t n) {
   p->amg_seed = 0;
   p->agg_dist0 = 2;
   p->agg_dist = 2;
+  p->cheb_fused = 1;
 }
 
 int seaice_create(const seaice_params* p, const seaice_runtime* rt, seaice_ctx** out) {

@@ -704,7 +704,7 @@ __host__ __device__ constexpr double mode_c(int a, int c) { return c == 0 ? xi_a
 // Per-step constants of the modal element algebra, computed on the host so the kernel reads
 // them as constant-bank operands (no registers, no device divisions).
 struct ElemK {
-  double al, be, al2, be2, sc, pp11, pp13, pp22, w, wdt, co, dtco, dmin2, prf, hb;
+  double al, be, al2, be2, sc, pp11, pp13, pp22, w, wdt, co, dtco, dmin2, prf, hb, dt, inv_dx;
 };
 static ElemK make_elemk(const Phys& ph) {
   ElemK k;
@@ -724,6 +724,8 @@ static ElemK make_elemk(const Phys& ph) {
   k.dmin2 = ph.delta_min * ph.delta_min;
   k.prf = k.wdt * inv_dx;
   k.hb = 0.5 * k.wdt * inv_dx;
+  k.dt = ph.dt;
+  k.inv_dx = inv_dx;
   return k;
 }
 
@@ -735,30 +737,16 @@ __device__ __forceinline__ void element_modal(const Phys& ph, const ElemK& K, in
   const int n = ph.n, s = n + 1;
   const long long Nc = (long long)n * n;
   const int cell = cj * n + ci;
-  // Modal coefficients of the nodal fields: u(xi, eta) = m0 + m1 xi + m2 eta + m3 xi eta
-  // (nodes CCW from (-1,-1)); grad u = (2/dx) (m1 + m3 eta, m2 + m3 xi).
-  double mu[4][2], mw[4][2];  // velocity v and ocean-relative velocity v_o - v
+  double u[4][2], dw[4][2];  // nodal velocity v and ocean-relative velocity v_o - v
   {
     const int nd0 = cj * s + ci;
     const int ids[4] = {nd0, nd0 + 1, nd0 + s + 1, nd0 + s};
-    double u[4][2], dw[4][2];
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const double2 a1 = __ldg(reinterpret_cast<const double2*>(v) + ids[b]);
       const double2 a2 = __ldg(reinterpret_cast<const double2*>(vo) + ids[b]);
       u[b][0] = a1.x; u[b][1] = a1.y;
       dw[b][0] = a2.x - a1.x; dw[b][1] = a2.y - a1.y;
-    }
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      mu[0][c] = 0.25 * ((u[0][c] + u[2][c]) + (u[1][c] + u[3][c]));
-      mu[1][c] = 0.25 * ((u[1][c] + u[2][c]) - (u[0][c] + u[3][c]));
-      mu[2][c] = 0.25 * ((u[2][c] + u[3][c]) - (u[0][c] + u[1][c]));
-      mu[3][c] = 0.25 * ((u[0][c] + u[2][c]) - (u[1][c] + u[3][c]));
-      mw[0][c] = 0.25 * ((dw[0][c] + dw[2][c]) + (dw[1][c] + dw[3][c]));
-      mw[1][c] = 0.25 * ((dw[1][c] + dw[2][c]) - (dw[0][c] + dw[3][c]));
-      mw[2][c] = 0.25 * ((dw[2][c] + dw[3][c]) - (dw[0][c] + dw[1][c]));
-      mw[3][c] = 0.25 * ((dw[0][c] + dw[2][c]) - (dw[1][c] + dw[3][c]));
     }
   }
   const double Pc = P[cell], rh = rhoh[cell];
@@ -768,9 +756,12 @@ __device__ __forceinline__ void element_modal(const Phys& ph, const ElemK& K, in
   constexpr double g2 = 1.0 / 3.0;
   // The per-Gauss-point Q_ij and drag coefficients are parked in this thread's 36 Ks slots
   // (slot 9q + j) and combined after the loop: that keeps the loop's live state small.
-  // Residual moments: F_k = sum_q f_k (1, xi, eta, xi eta), B = sums of c0 b_i (see below).
-  double fx0 = 0, fx1 = 0, fx2 = 0, fx3 = 0, fy0 = 0, fy1 = 0, fy2 = 0, fy3 = 0;
-  double B1 = 0, B2 = 0, B3 = 0, B4 = 0, B5 = 0;
+  // The residual is accumulated directly per Gauss point (nodal interpolation, the same
+  // grouping as the per-node residual kernel): it decides Newton convergence at 1e-8, so it
+  // keeps the smallest rounding error rather than the cheapest modal form.
+  double Ra[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) Ra[p] = 0.0;
   // pi of the next Gauss point is fetched one iteration ahead (software pipelining)
   double pn0 = 0.0, pn1 = 0.0, pn2 = 0.0;
   if (KIND == SEAICE_JAC_SV) {
@@ -778,19 +769,24 @@ __device__ __forceinline__ void element_modal(const Phys& ph, const ElemK& K, in
   }
 #pragma unroll 1
   for (int q = 0; q < 4; ++q) {
-    const double xq = xi_q(q), eq = eta_q(q), xe = xq * eq;
     const double p11 = pn0, p12 = pn1, p22 = pn2;
     if (KIND == SEAICE_JAC_SV && q < 3) {
       pn0 = __ldg(pi + (q + 1) * Nc + cell); pn1 = __ldg(pi + (5 + q) * Nc + cell); pn2 = __ldg(pi + (9 + q) * Nc + cell);
     }
-    const double vx = mu[0][0] + mu[1][0] * xq + mu[2][0] * eq + mu[3][0] * xe;
-    const double vy = mu[0][1] + mu[1][1] * xq + mu[2][1] * eq + mu[3][1] * xe;
-    const double wx = mw[0][0] + mw[1][0] * xq + mw[2][0] * eq + mw[3][0] * xe;
-    const double wy = mw[0][1] + mw[1][1] * xq + mw[2][1] * eq + mw[3][1] * xe;
-    // reference-scaled gradient (physical = 2/dx times this)
-    const double L00 = mu[1][0] + mu[3][0] * eq, L01 = mu[2][0] + mu[3][0] * xq;
-    const double L10 = mu[1][1] + mu[3][1] * eq, L11 = mu[2][1] + mu[3][1] * xq;
-    const double tx = al2 * (L00 + L11), ty = be2 * (L00 - L11), tz = be2 * (L01 + L10);  // tau^(v)
+    double vx = 0, vy = 0, wx = 0, wy = 0, L00 = 0, L01 = 0, L10 = 0, L11 = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      vx += Nq(q, b) * u[b][0];
+      vy += Nq(q, b) * u[b][1];
+      wx += Nq(q, b) * dw[b][0];
+      wy += Nq(q, b) * dw[b][1];
+      L00 += Gx(q, b) * u[b][0];
+      L01 += Gy(q, b) * u[b][0];
+      L10 += Gx(q, b) * u[b][1];
+      L11 += Gy(q, b) * u[b][1];
+    }
+    // (Gx, Gy are reference gradients x 2: physical = 0.5 * (2/dx) * G)
+    const double tx = 0.5 * al2 * (L00 + L11), ty = 0.5 * be2 * (L00 - L11), tz = 0.5 * be2 * (L01 + L10);
     const double X = dmin2 + 2.0 * (tx * tx + ty * ty + tz * tz);  // Delta^2 >= Delta_min^2 > 0
     const double rD = rsqrt(X);                                      // 1/Delta
     const double c0 = Pc * rD;
@@ -834,28 +830,21 @@ __device__ __forceinline__ void element_modal(const Phys& ph, const ElemK& K, in
     }
     const double d00 = co * nw + inw * wx * wx, d11 = co * nw + inw * wy * wy, d01 = inw * wx * wy;
     slot[6 * kTC] = wdt * d00; slot[7 * kTC] = wdt * d11; slot[8 * kTC] = wdt * d01;
-    // residual moments (mass + drag part f_k, stress part c0 b_i)
-    const double fx = w * (rh * vx - K.dtco * nw * wx), fy = w * (rh * vy - K.dtco * nw * wy);
-    fx0 += fx; fx1 += xq * fx; fx2 += eq * fx; fx3 += xe * fx;
-    fy0 += fy; fy1 += xq * fy; fy2 += eq * fy; fy3 += xe * fy;
-    const double e1 = c0 * b1, e2 = c0 * b2, e3 = c0 * b3;
-    B1 += e1; B2 += e2; B3 += e3;
-    B4 += eq * e1 + xq * e2;
-    B5 += xq * e3 + eq * e2;
+    // element residual -A(v, phi_{a,k}) (eq:A), term by term as in the per-node kernel
+    const double dtc0 = K.dt * c0, hp = 0.5 * K.dt * Pc, dcn = K.dtco * nw;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const double Na = Nq(q, a), gx = Gx(q, a) * K.inv_dx, gy = Gy(q, a) * K.inv_dx;
+      const double tdx = gx * b1 + gy * b2;  // tau^(v) . tau^(N_a e_x)
+      const double tdy = gy * b3 + gx * b2;  // tau^(v) . tau^(N_a e_y)
+      Ra[2 * a] += -w * (rh * vx * Na + dtc0 * tdx - hp * gx - dcn * wx * Na);
+      Ra[2 * a + 1] += -w * (rh * vy * Na + dtc0 * tdy - hp * gy - dcn * wy * Na);
+    }
   }
-  // element residual -A(v, phi_{a,k}):
-  //   -sum_q N_a f_k = -(F0 + X F1 + Y F2 + XY F3)/4,
-  //   -sum_q w dt c0 tau^(v).tau^(N_a e_k) = -(w dt/(2dx)) (X B1 + Y B2 + XY B4)  (k = x)
-  //                                          -(w dt/(2dx)) (Y B3 + X B2 + XY B5)  (k = y),
-  //   + w dt (P/2) sum_q dN_a/dx_k = w dt P X/dx (resp. Y).
-  const double pr = K.prf * Pc, hb = K.hb;
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    const double X = xi_a(a), Y = eta_a(a), XY = xe_a(a);
-    const double rx = -(0.25 * (fx0 + X * fx1 + Y * fx2 + XY * fx3) + hb * (X * B1 + Y * B2 + XY * B4)) + pr * X;
-    const double ry = -(0.25 * (fy0 + X * fy1 + Y * fy2 + XY * fy3) + hb * (Y * B3 + X * B2 + XY * B5)) + pr * Y;
-    Rs[(2 * a) * kTC + t] = rx;
-    Rs[(2 * a + 1) * kTC + t] = ry;
+    Rs[(2 * a) * kTC + t] = Ra[2 * a];
+    Rs[(2 * a + 1) * kTC + t] = Ra[2 * a + 1];
   }
   // accumulate S (15 distinct entries) and the drag moments from the parked values
   double s00 = 0, s01 = 0, s02 = 0, s11 = 0, s12 = 0, s22 = 0, s04 = 0, s05 = 0, s14 = 0, s15 = 0, s24 = 0,

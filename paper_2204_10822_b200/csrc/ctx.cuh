@@ -95,6 +95,7 @@ enum ProfClass {
   PC_COARSE = 10,   // K6 dense coarse solve
   PC_RESIDC = 11,   // residual + Dinv, coarse levels
   PC_PIUPD = 12,    // K12 dual update
+  PC_CHEB0F = 13,   // K4 three Chebyshev steps fused (temporal blocking), finest level
   PC_NCLASS = 16
 };
 struct Prof {

@@ -8,6 +8,7 @@
 // Everything is deterministic: integer atomics only produce counts/flags, sorting uses
 // CUB's stable radix / segmented sorts, SpGEMM accumulates each output block in a fixed
 // (row-major product) order by a single thread, reductions are fixed-order two-stage.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -17,6 +18,7 @@
 #include "ctx.cuh"
 
 namespace seaice {
+namespace cg = cooperative_groups;
 
 void bsr_apply(Ctx& c, int nb, int br, int bc, const int* rp, const int* ci, const double* val, const double* x,
                double* y);
@@ -1160,20 +1162,27 @@ __global__ void __launch_bounds__(256) k_cheb_stencil(int n, int Nn, const doubl
   }
 }
 
-// Three Chebyshev steps fused (temporal blocking) on the stencil level.  A CTA owns a
-// kF x kF tile of nodes and one thread per node of the tile plus two rings (32 x 32): d_0 is
-// staged in shared memory on the tile plus three rings, step k (k = 1, 2, 3) updates the nodes
-// within 3 - k rings of the tile (its A d_{k-1} needs d_{k-1} one ring further out), and d_k
-// goes back to shared memory.  r and the x increment stay in registers (pointwise).  The
-// stencil is read from HBM once per fused launch (steps 2 and 3 re-read it from L2) instead of
-// once per step, so a 3-step smoothing moves ~2.3x fewer bytes.  Same arithmetic per node and
-// step as three k_cheb_stencil launches.
-//   x_3 = x_0 + d_0 + d_1 + d_2 (x_0 = 0 if first);  r_k = r_{k-1} - A d_{k-1};
-//   d_k = c1[k] d_{k-1} + c2[k] Dinv r_k (k = 1, 2);  r_3 written iff want_r3.
-constexpr int kF = 28, kFR = kF + 4, kFH = kF + 6;        // tile, tile + 2 rings, tile + 3 rings (x)
-constexpr int kFY = 4, kFRY = kFY + 4, kFHY = kFY + 6;     // same in y
-struct Cheb3Coef {
-  double c1[2], c2[2];
+// M Chebyshev steps fused (temporal blocking) on the stencil level.  A CTA owns a
+// TX x 4 tile of nodes (TX = 34 - 2M, so tile + M-1 rings is 32 nodes = one warp wide) and one
+// thread per node of the tile plus M-1 rings: d_0 is staged in shared memory on the tile plus M
+// rings, step k (k = 1..M) updates the nodes within M - k rings of the tile (its A d_{k-1}
+// needs d_{k-1} one ring further out), and d_k goes back to shared memory.  Each thread keeps
+// its node's stencil row (36 values), r and the x increment in registers, so the stencil is
+// read from memory once per fused launch instead of once per step (halo rows shared with the
+// neighbouring tiles mostly hit L2).  Same arithmetic per node and step as M k_cheb_stencil
+// launches:  x_M = x_0 + d_0 + ... + d_{M-1} (x_0 = 0 if first);  r_k = r_{k-1} - A d_{k-1};
+// d_k = c1[k] d_{k-1} + c2[k] Dinv r_k (k < M);  r_M written (out of place) iff want_rM.
+constexpr int kFW = 32, kFY = 4;  // threads per row (tile + rings), tile rows
+constexpr int kFMaxM = 6;
+template <int M> struct FusedGeom {
+  static constexpr int R = M - 1;             // rings computed around the tile
+  static constexpr int TX = kFW - 2 * R;      // tile width
+  static constexpr int RY = kFY + 2 * R;      // rows of tile + R rings
+  static constexpr int HX = TX + 2 * M, HY = kFY + 2 * M;  // d staging region (tile + M rings)
+  static constexpr int NT = kFW * RY;         // threads
+};
+struct ChebFCoef {
+  double c1[kFMaxM], c2[kFMaxM];
 };
 // y = A d at this thread's node, stencil row in registers, d from shared memory
 __device__ __forceinline__ double2 stencil_apply_reg(bool interior, const double (&Jr)[36],
@@ -1194,26 +1203,26 @@ __device__ __forceinline__ double2 stencil_apply_reg(bool interior, const double
   return make_double2(y0, y1);
 }
 
-__global__ void __launch_bounds__(kFR * kFRY, 2) k_cheb3_stencil(int n, int Nn, const double* __restrict__ J,
-                                                                const double* __restrict__ dinv,
-                                                                const double2* __restrict__ d,
-                                                                const double2* __restrict__ rin,
-                                                                double2* __restrict__ rout, double2* __restrict__ x,
-                                                                Cheb3Coef k, int first, int want_r3) {
-  __shared__ double2 sd[2][kFH * kFHY];
+template <int M>
+__global__ void __launch_bounds__(FusedGeom<M>::NT, (FusedGeom<M>::NT <= 256 ? 2 : 1))
+    k_chebM_stencil(int n, int Nn, const double* __restrict__ J, const double* __restrict__ dinv,
+                    const double2* __restrict__ d, const double2* __restrict__ rin, double2* __restrict__ rout,
+                    double2* __restrict__ x, ChebFCoef k, int first, int want_rM) {
+  using Gm = FusedGeom<M>;
+  __shared__ double2 sd[2][Gm::HX * Gm::HY];
   const int s = n + 1;
-  const int i0 = blockIdx.x * kF, j0 = blockIdx.y * kFY;
+  const int i0 = blockIdx.x * Gm::TX, j0 = blockIdx.y * kFY;
   const int t = threadIdx.x;
-  const int li = t % kFR, lj = t / kFR;  // position in the tile + 2 rings
-  const int gi = i0 - 2 + li, gj = j0 - 2 + lj;
-  const int di = li < 2 ? 2 - li : (li >= kF + 2 ? li - (kF + 1) : 0);
-  const int dj = lj < 2 ? 2 - lj : (lj >= kFY + 2 ? lj - (kFY + 1) : 0);
+  const int li = t % kFW, lj = t / kFW;  // position in the tile + R rings
+  const int gi = i0 - Gm::R + li, gj = j0 - Gm::R + lj;
+  const int di = li < Gm::R ? Gm::R - li : (li >= Gm::TX + Gm::R ? li - (Gm::TX + Gm::R - 1) : 0);
+  const int dj = lj < Gm::R ? Gm::R - lj : (lj >= kFY + Gm::R ? lj - (kFY + Gm::R - 1) : 0);
   const int depth = di > dj ? di : dj;  // ring index (0 = tile)
   const bool inside = gi >= 0 && gi <= n && gj >= 0 && gj <= n;
   const int node = gj * s + gi;
   const bool interior = gi > 0 && gi < n && gj > 0 && gj < n;
-  const int sidx = (lj + 1) * kFH + (li + 1);
-  // this node's stencil row (read once for the three steps), r_0, Dinv, x_0
+  const int sidx = (lj + 1) * Gm::HX + (li + 1);
+  // this node's stencil row (read once for the M steps), r_0, Dinv, x_0
   double Jr[36];
   double2 rv = make_double2(0.0, 0.0), xa = make_double2(0.0, 0.0);
   double4 D = make_double4(0.0, 0.0, 0.0, 0.0);
@@ -1232,20 +1241,20 @@ __global__ void __launch_bounds__(kFR * kFRY, 2) k_cheb3_stencil(int n, int Nn, 
 #pragma unroll
     for (int e = 0; e < 36; ++e) Jr[e] = 0.0;
   }
-  // stage d_0 on the tile + 3 rings (zero outside the domain)
-  for (int idx = t; idx < kFH * kFHY; idx += kFR * kFRY) {
-    const int hi = i0 - 3 + idx % kFH, hj = j0 - 3 + idx / kFH;
+  // stage d_0 on the tile + M rings (zero outside the domain)
+  for (int idx = t; idx < Gm::HX * Gm::HY; idx += Gm::NT) {
+    const int hi = i0 - M + idx % Gm::HX, hj = j0 - M + idx / Gm::HX;
     sd[0][idx] = (hi >= 0 && hi <= n && hj >= 0 && hj <= n) ? d[hj * s + hi] : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  // steps 1 and 2
+  // steps 1 .. M-1
 #pragma unroll
-  for (int st = 0; st < 2; ++st) {
+  for (int st = 0; st < M - 1; ++st) {
     const double2* din = sd[st & 1];
     double2* dnx = sd[(st + 1) & 1];
-    if (inside && depth <= 2 - st) {
+    if (inside && depth <= M - 1 - st) {
       const double2 dv = din[sidx];
-      const double2 y = stencil_apply_reg(interior, Jr, din, sidx, kFH);
+      const double2 y = stencil_apply_reg(interior, Jr, din, sidx, Gm::HX);
       rv.x -= y.x;
       rv.y -= y.y;
       xa.x += dv.x;
@@ -1255,20 +1264,30 @@ __global__ void __launch_bounds__(kFR * kFRY, 2) k_cheb3_stencil(int n, int Nn, 
     }
     __syncthreads();
   }
-  // step 3 (tile only): x += d_2; r -= A d_2 if wanted
+  // step M (tile only): x += d_{M-1}; r -= A d_{M-1} if wanted
   if (inside && depth == 0) {
-    const double2* din = sd[0];
+    const double2* din = sd[(M - 1) & 1];
     const double2 dv = din[sidx];
     xa.x += dv.x;
     xa.y += dv.y;
     x[node] = xa;
-    if (want_r3) {
-      const double2 y = stencil_apply_reg(interior, Jr, din, sidx, kFH);
+    if (want_rM) {
+      const double2 y = stencil_apply_reg(interior, Jr, din, sidx, Gm::HX);
       rv.x -= y.x;
       rv.y -= y.y;
       rout[node] = rv;  // out of place: neighbouring CTAs still read r_0 in their halo
     }
   }
+}
+
+template <int M>
+static void launch_chebM(Ctx& c, const double* dinv, const double* d, const double* r, double* rout, double* x,
+                         const ChebFCoef& kc, bool pre) {
+  using Gm = FusedGeom<M>;
+  const dim3 grid((c.n + 1 + Gm::TX - 1) / Gm::TX, (c.n + 1 + kFY - 1) / kFY);
+  k_chebM_stencil<M><<<grid, Gm::NT, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), dinv, (const double2*)d,
+                                                (const double2*)r, (double2*)rout, (double2*)x, kc, pre ? 1 : 0,
+                                                pre ? 1 : 0);
 }
 
 // r = b - A x (or r = b if x == NULL); d = Dinv r * c2 (stencil level)
@@ -1589,6 +1608,164 @@ static int ggrid(int nb, int G) { return (int)(((long long)nb * G + 255) / 256);
     default: { constexpr int GG = 32; CALL; } break; \
   }
 
+// ------------------------------------------------------------------ coarse tail (persistent)
+// The small coarse levels (A resident in L2) cost one launch latency per kernel, ~10 kernels
+// per level and V-cycle.  Below Ctx::tail_start the whole V-cycle (pre-smoothing, restriction,
+// dense coarsest solve, prolongation, post-smoothing) runs in ONE cooperative launch with a
+// grid-wide barrier between dependent phases; each phase is the same per-row arithmetic as
+// the corresponding k_gresid / k_gcheb / k_gspmv launch (same group size, same order).
+constexpr int kTailMaxLev = 10, kTailMaxDeg = 8;
+struct TailLevel {
+  int nb, nbc, GA, GR, GP;
+  const int *rp, *ci, *Rrp, *Rci, *Prp, *Pci;
+  const double *valT, *dinv, *RvalT, *PvalT;
+  double *x, *rhs, *r, *d, *d2;
+  double ith;                                 // 1 / theta
+  double c1[kTailMaxDeg], c2[kTailMaxDeg];    // Chebyshev step coefficients
+};
+struct TailArgs {
+  int nl, m, cn;
+  const double* cinv;
+  TailLevel L[kTailMaxLev];
+};
+
+template <int G>
+__device__ __forceinline__ void tail_resid(const TailLevel& L, const double* __restrict__ b,
+                                           const double* __restrict__ x, long long gt, long long gs) {
+  const long long tot = ((long long)L.nb * G + 31) / 32 * 32;
+  for (long long tt = gt; tt < tot; tt += gs) {
+    const int row = (int)(tt / G), lig = (int)(tt % G);
+    const bool own = row < L.nb && lig < 3;
+    const long long i = (long long)row * 3 + lig;
+    double bo = 0.0, D[3] = {0.0, 0.0, 0.0};
+    if (own) {
+      bo = b[i];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) D[k] = L.dinv[(long long)row * 9 + lig * 3 + k];
+    }
+    double acc[3];
+    if (x) grp_row<3, 3, G>(row, L.nb, lig, L.rp, L.ci, L.valT, x, acc);
+    else acc[0] = acc[1] = acc[2] = 0.0;
+    const double rv = bo - (own ? pick<3>(acc, lig) : 0.0);
+    if (own) L.r[i] = rv;
+    double z = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) z += D[k] * __shfl_sync(0xffffffffu, rv, k, G);
+    if (own) L.d[i] = L.ith * z;
+  }
+}
+
+template <int G>
+__device__ __forceinline__ void tail_cheb(const TailLevel& L, const double* __restrict__ d,
+                                          double* __restrict__ dout, double c1, double c2, int first, int want_r,
+                                          int want_d, long long gt, long long gs) {
+  const long long tot = ((long long)L.nb * G + 31) / 32 * 32;
+  for (long long tt = gt; tt < tot; tt += gs) {
+    const int row = (int)(tt / G), lig = (int)(tt % G);
+    double acc[3];
+    if (want_r) grp_row<3, 3, G>(row, L.nb, lig, L.rp, L.ci, L.valT, d, acc);
+    if (row >= L.nb || lig != 0) continue;
+    double dv[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const long long i = (long long)row * 3 + a;
+      dv[a] = d[i];
+      L.x[i] = (first ? 0.0 : L.x[i]) + dv[a];
+    }
+    if (!want_r) continue;
+    double rv[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const long long i = (long long)row * 3 + a;
+      rv[a] = L.r[i] - acc[a];
+      L.r[i] = rv[a];
+    }
+    if (want_d) {
+      const double* D = L.dinv + (long long)row * 9;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        double z = 0.0;
+#pragma unroll
+        for (int b = 0; b < 3; ++b) z += D[a * 3 + b] * rv[b];
+        dout[(long long)row * 3 + a] = c1 * dv[a] + c2 * z;
+      }
+    }
+  }
+}
+
+template <int G>
+__device__ __forceinline__ void tail_spmv(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                                          const double* __restrict__ val, const double* __restrict__ x,
+                                          double* __restrict__ y, int add, long long gt, long long gs) {
+  const long long tot = ((long long)nb * G + 31) / 32 * 32;
+  for (long long tt = gt; tt < tot; tt += gs) {
+    const int row = (int)(tt / G), lig = (int)(tt % G);
+    const bool own = row < nb && lig < 3;
+    const long long i = (long long)row * 3 + lig;
+    const double y0 = (own && add) ? y[i] : 0.0;
+    double acc[3];
+    grp_row<3, 3, G>(row, nb, lig, rp, ci, val, x, acc);
+    if (own) y[i] = y0 + pick<3>(acc, lig);
+  }
+}
+
+#define SI_TDISPATCH(G, CALL) \
+  switch (G) {                \
+    case 4: { constexpr int GG = 4; CALL; } break;   \
+    case 8: { constexpr int GG = 8; CALL; } break;   \
+    case 16: { constexpr int GG = 16; CALL; } break; \
+    default: { constexpr int GG = 32; CALL; } break; \
+  }
+
+__global__ void __launch_bounds__(512, 1) k_vcycle_tail(const __grid_constant__ TailArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long gs = (long long)gridDim.x * blockDim.x;
+  const int nl = A.nl, m = A.m;
+  for (int l = 0; l < nl - 1; ++l) {  // down: pre-smoothing from x = 0, restriction
+    const TailLevel& L = A.L[l];
+    SI_TDISPATCH(L.GA, (tail_resid<GG>(L, L.rhs, nullptr, gt, gs)));
+    grid.sync();
+    double* d = L.d;
+    double* d2 = L.d2;
+    for (int it = 0; it < m; ++it) {
+      const int want_d = (it < m - 1) ? 1 : 0;
+      SI_TDISPATCH(L.GA, (tail_cheb<GG>(L, d, d2, L.c1[it], L.c2[it], it == 0 ? 1 : 0, 1, want_d, gt, gs)));
+      grid.sync();
+      double* tp = d; d = d2; d2 = tp;
+    }
+    SI_TDISPATCH(L.GR, (tail_spmv<GG>(L.nbc, L.Rrp, L.Rci, L.RvalT, L.r, A.L[l + 1].rhs, 0, gt, gs)));
+    grid.sync();
+  }
+  {  // dense coarsest solve x = C^-1 b (warp per row)
+    const TailLevel& Lc = A.L[nl - 1];
+    const long long nw = gs >> 5;
+    const int lane = threadIdx.x & 31;
+    for (long long w = gt >> 5; w < A.cn; w += nw) {
+      double sacc = 0.0;
+      for (int k = lane; k < A.cn; k += 32) sacc += A.cinv[w * A.cn + k] * Lc.rhs[k];
+      sacc = warp_sum(sacc);
+      if (lane == 0) Lc.x[w] = sacc;
+    }
+    grid.sync();
+  }
+  for (int l = nl - 2; l >= 0; --l) {  // up: prolongation, post-smoothing
+    const TailLevel& L = A.L[l];
+    SI_TDISPATCH(L.GP, (tail_spmv<GG>(L.nb, L.Prp, L.Pci, L.PvalT, A.L[l + 1].x, L.x, 1, gt, gs)));
+    grid.sync();
+    SI_TDISPATCH(L.GA, (tail_resid<GG>(L, L.rhs, L.x, gt, gs)));
+    grid.sync();
+    double* d = L.d;
+    double* d2 = L.d2;
+    for (int it = 0; it < m; ++it) {
+      const int last = (it == m - 1) ? 1 : 0;
+      SI_TDISPATCH(L.GA, (tail_cheb<GG>(L, d, d2, L.c1[it], L.c2[it], 0, !last, !last, gt, gs)));
+      grid.sync();
+      double* tp = d; d = d2; d2 = tp;
+    }
+  }
+}
+
 static void gspmv(Ctx& c, int nb, int br, int bc, long long nnzb, const int* rp, const int* ci, const double* val,
                   const double* x, double* y, int add) {
   const int G = pick_group(nnzb, nb);
@@ -1898,6 +2075,23 @@ void amg_setup_impl(Ctx& c) {
   SI_CHECK(!(flag & 4), SEAICE_ENONFINITE, "AMG: singular diagonal block");
   SI_CHECK(!(flag & 8), SEAICE_ENONFINITE, "AMG: coarse matrix not positive definite");
   c.op_complexity = (double)nnz_total / (double)nnz0;
+  // persistent coarse tail: the levels >= tail_start (all b = 3, DOFs <= coarse_tail_dof)
+  c.tail_start = 0;
+  if (c.p.coarse_tail_dof > 0 && c.p.cheb_degree <= kTailMaxDeg) {
+    for (int l = 1; l < c.nlev; ++l) {
+      if ((long long)c.lv[l].nb * c.lv[l].b <= c.p.coarse_tail_dof) {
+        if (c.nlev - l <= kTailMaxLev && l < c.nlev - 1) c.tail_start = l;
+        break;
+      }
+    }
+  }
+  if (c.tail_start > 0 && c.tail_grid == 0) {
+    int dev = 0, sms = 0, per = 0;
+    SI_CUDA(cudaGetDevice(&dev));
+    SI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    SI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_vcycle_tail, 512, 0));
+    c.tail_grid = sms * (per < 1 ? 1 : per);
+  }
   c.amg_ready = true;
 }
 
@@ -1917,7 +2111,7 @@ static ChebCoef cheb_coef(const Ctx& c, const Level& L) {
 // One Chebyshev smoothing on level l for A x = b.  pre: x = 0 start, leaves r = b - A x.
 static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
   Level& L = c.lv[l];
-  const int m = c.p.cheb_degree;
+  const int m = (l == 0 && c.p.cheb_degree0 > 0) ? c.p.cheb_degree0 : c.p.cheb_degree;
   const ChebCoef k = cheb_coef(c, L);
   double rho = 1.0 / k.sg;
   double* r = L.r.get();
@@ -1943,21 +2137,23 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
     if (!pre) by += L.nnzb * (8.0 * B * B + (st ? 0.0 : 4.0)) + (st ? 0.0 : 4.0 * (L.nb + 1)) + 8.0 * B * L.nb;
     prof_end(c, st ? PC_RESID0 : PC_RESIDC, by);
   }
-  if (st && m == 3 && c.p.cheb_fused) {
-    Cheb3Coef kc;
-    for (int it = 0; it < 2; ++it) {
+  if (st && m >= 3 && m <= kFMaxM && c.p.cheb_fused) {
+    ChebFCoef kc;
+    for (int it = 0; it < m - 1; ++it) {
       const double rho_new = 1.0 / (2.0 * k.sg - rho);
       kc.c1[it] = rho_new * rho;
       kc.c2[it] = 2.0 * rho_new / k.de;
       rho = rho_new;
     }
     prof_begin(c);
-    const dim3 grid((c.n + 1 + kF - 1) / kF, (c.n + 1 + kFY - 1) / kFY);
-    k_cheb3_stencil<<<grid, kFR * kFRY, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L.dinv.get(), (const double2*)d,
-                                                  (const double2*)r, (double2*)d2, (double2*)x, kc, pre ? 1 : 0,
-                                                  pre ? 1 : 0);
+    switch (m) {
+      case 3: launch_chebM<3>(c, L.dinv.get(), d, r, d2, x, kc, pre); break;
+      case 4: launch_chebM<4>(c, L.dinv.get(), d, r, d2, x, kc, pre); break;
+      case 5: launch_chebM<5>(c, L.dinv.get(), d, r, d2, x, kc, pre); break;
+      default: launch_chebM<6>(c, L.dinv.get(), d, r, d2, x, kc, pre); break;
+    }
     SI_LAUNCHED(c);
-    if (pre) std::swap(L.r, L.d2);  // r_3 was written to d2
+    if (pre) std::swap(L.r, L.d2);  // r_M was written to d2
     // algorithmic bytes: stencil + Dinv once, d_0 / r_0 / x_0 read, x (and r) written
     prof_end(c, PC_CHEB0F, (double)c.Nn * (288.0 + 32.0 + 16.0 * 2 + (pre ? 0.0 : 16.0) + 16.0 + (pre ? 16.0 : 0.0)));
     return;
@@ -1993,8 +2189,52 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
   }
 }
 
+static void vcycle_tail(Ctx& c) {
+  const int l0 = c.tail_start;
+  TailArgs A;
+  A.nl = c.nlev - l0;
+  A.m = c.p.cheb_degree;
+  A.cn = c.cn;
+  A.cinv = c.cinv.get();
+  double bytes = 8.0 * c.cn * c.cn;
+  for (int k = 0; k < A.nl; ++k) {
+    Level& L = c.lv[l0 + k];
+    TailLevel& T = A.L[k];
+    T.nb = L.nb;
+    T.nbc = L.nbc;
+    T.GA = pick_group(L.nnzb, L.nb);
+    T.GR = pick_group(L.Rnnzb, L.nbc);
+    T.GP = pick_group(L.Pnnzb, L.nb);
+    T.rp = L.rp.get(); T.ci = L.ci.get(); T.valT = L.valT.get(); T.dinv = L.dinv.get();
+    T.Rrp = L.Rrp.get(); T.Rci = L.Rci.get(); T.RvalT = L.RvalT.get();
+    T.Prp = L.Prp.get(); T.Pci = L.Pci.get(); T.PvalT = L.PvalT.get();
+    T.x = L.x.get(); T.rhs = L.rhs.get(); T.r = L.r.get(); T.d = L.d.get(); T.d2 = L.d2.get();
+    if (k == A.nl - 1) break;  // coarsest: dense solve only
+    const ChebCoef kc = cheb_coef(c, L);
+    T.ith = 1.0 / kc.th;
+    double rho = 1.0 / kc.sg;
+    for (int it = 0; it < A.m; ++it) {
+      const double rho_new = 1.0 / (2.0 * kc.sg - rho);
+      T.c1[it] = rho_new * rho;
+      T.c2[it] = 2.0 * rho_new / kc.de;
+      rho = rho_new;
+    }
+    // A read (2m + 1) times, R and P once, ~10 vector passes
+    bytes += (2.0 * A.m + 1.0) * L.nnzb * 76.0 + (L.Rnnzb + L.Pnnzb) * 76.0 + 10.0 * 24.0 * L.nb;
+  }
+  prof_begin(c);
+  void* args[] = {(void*)&A};
+  SI_CUDA(cudaLaunchCooperativeKernel((const void*)k_vcycle_tail, dim3(c.tail_grid), dim3(512), args, 0, c.s));
+  SI_LAUNCHED(c);
+  prof_end(c, PC_TAIL, bytes);
+}
+
 static void vcycle_level(Ctx& c, int l, const double* b, double* x) {
   Level& L = c.lv[l];
+  if (l > 0 && l == c.tail_start) {  // b = L.rhs, x = L.x
+    vcycle_tail(c);
+    return;
+  }
   if (l + 1 == c.nlev) {
     prof_begin(c);
     k_dense_gemv<<<grid_for((long long)c.cn * 32, 256), 256, 0, c.s>>>(c.cn, c.cinv.get(), b, x);

@@ -1162,27 +1162,31 @@ __global__ void __launch_bounds__(256) k_cheb_stencil(int n, int Nn, const doubl
   }
 }
 
-// M Chebyshev steps fused (temporal blocking) on the stencil level.  A CTA owns a
-// TX x 4 tile of nodes (TX = 34 - 2M, so tile + M-1 rings is 32 nodes = one warp wide) and one
-// thread per node of the tile plus M-1 rings: d_0 is staged in shared memory on the tile plus M
-// rings, step k (k = 1..M) updates the nodes within M - k rings of the tile (its A d_{k-1}
-// needs d_{k-1} one ring further out), and d_k goes back to shared memory.  Each thread keeps
-// its node's stencil row (36 values), r and the x increment in registers, so the stencil is
-// read from memory once per fused launch instead of once per step (halo rows shared with the
-// neighbouring tiles mostly hit L2).  Same arithmetic per node and step as M k_cheb_stencil
-// launches:  x_M = x_0 + d_0 + ... + d_{M-1} (x_0 = 0 if first);  r_k = r_{k-1} - A d_{k-1};
-// d_k = c1[k] d_{k-1} + c2[k] Dinv r_k (k < M);  r_M written (out of place) iff want_rM.
+// Chebyshev(M) smoothing on the stencil level in one launch (temporal blocking).  A CTA owns
+// a TX x 4 tile of nodes (TX = 34 - 2M, so tile + M-1 rings is 32 nodes = one warp wide) and
+// one thread per node of the tile plus M-1 rings; each thread keeps its node's stencil row (36
+// values), r and the x increment in registers.  d_0 lives in shared memory on the tile plus M
+// rings: for pre-smoothing (x_0 = 0) it is built in the kernel, r_0 = b, d_0 = ith Dinv b
+// (pointwise); for post-smoothing it is staged from d0g (written by k_resid_dinv_stencil with
+// r_0 = rin).  Step k (k = 1..M) then updates the nodes within M - k rings of the tile (its
+// A d_{k-1} needs d_{k-1} one ring further out) and writes d_k back to shared memory.  The
+// stencil is read from HBM once per smoothing step group instead of once per step (halo rows
+// shared with neighbouring tiles mostly hit L2).  Same arithmetic per node and step as
+// k_resid_dinv_stencil (pre) followed by M k_cheb_stencil launches:
+//   x_M = x_0 + d_0 + ... + d_{M-1};  r_k = r_{k-1} - A d_{k-1};
+//   d_k = c1[k] d_{k-1} + c2[k] Dinv r_k (k < M);  r_M written (out of place) iff pre.
 constexpr int kFW = 32, kFY = 4;  // threads per row (tile + rings), tile rows
 constexpr int kFMaxM = 6;
 template <int M> struct FusedGeom {
   static constexpr int R = M - 1;             // rings computed around the tile
   static constexpr int TX = kFW - 2 * R;      // tile width
   static constexpr int RY = kFY + 2 * R;      // rows of tile + R rings
-  static constexpr int HX = TX + 2 * M, HY = kFY + 2 * M;  // d staging region (tile + M rings)
+  static constexpr int HX = TX + 2 * M, HY = kFY + 2 * M;  // d region (tile + M rings)
   static constexpr int NT = kFW * RY;         // threads
 };
 struct ChebFCoef {
   double c1[kFMaxM], c2[kFMaxM];
+  double ith;  // 1 / theta
 };
 // y = A d at this thread's node, stencil row in registers, d from shared memory
 __device__ __forceinline__ double2 stencil_apply_reg(bool interior, const double (&Jr)[36],
@@ -1206,8 +1210,8 @@ __device__ __forceinline__ double2 stencil_apply_reg(bool interior, const double
 template <int M>
 __global__ void __launch_bounds__(FusedGeom<M>::NT, (FusedGeom<M>::NT <= 256 ? 2 : 1))
     k_chebM_stencil(int n, int Nn, const double* __restrict__ J, const double* __restrict__ dinv,
-                    const double2* __restrict__ d, const double2* __restrict__ rin, double2* __restrict__ rout,
-                    double2* __restrict__ x, ChebFCoef k, int first, int want_rM) {
+                    const double2* __restrict__ rin, const double2* __restrict__ d0g, double2* __restrict__ rout,
+                    double2* __restrict__ x, ChebFCoef k, int pre) {
   using Gm = FusedGeom<M>;
   __shared__ double2 sd[2][Gm::HX * Gm::HY];
   const int s = n + 1;
@@ -1236,15 +1240,34 @@ __global__ void __launch_bounds__(FusedGeom<M>::NT, (FusedGeom<M>::NT <= 256 ? 2
     }
     rv = rin[node];
     D = reinterpret_cast<const double4*>(dinv)[node];
-    if (depth == 0 && !first) xa = x[node];
+    if (depth == 0 && !pre) xa = x[node];
   } else {
 #pragma unroll
     for (int e = 0; e < 36; ++e) Jr[e] = 0.0;
   }
-  // stage d_0 on the tile + M rings (zero outside the domain)
-  for (int idx = t; idx < Gm::HX * Gm::HY; idx += Gm::NT) {
-    const int hi = i0 - M + idx % Gm::HX, hj = j0 - M + idx / Gm::HX;
-    sd[0][idx] = (hi >= 0 && hi <= n && hj >= 0 && hj <= n) ? d[hj * s + hi] : make_double2(0.0, 0.0);
+  if (pre) {  // d_0 = ith Dinv b on the tile + M rings
+    sd[0][sidx] = inside ? make_double2(k.ith * (D.x * rv.x + D.y * rv.y), k.ith * (D.z * rv.x + D.w * rv.y))
+                         : make_double2(0.0, 0.0);
+    for (int idx = t; idx < 2 * Gm::HX + 2 * (Gm::HY - 2); idx += Gm::NT) {  // outermost ring
+      int hx, hy;
+      if (idx < Gm::HX) { hx = idx; hy = 0; }
+      else if (idx < 2 * Gm::HX) { hx = idx - Gm::HX; hy = Gm::HY - 1; }
+      else { const int q = idx - 2 * Gm::HX; hx = (q & 1) ? Gm::HX - 1 : 0; hy = 1 + (q >> 1); }
+      const int hi = i0 - M + hx, hj = j0 - M + hy;
+      double2 dv = make_double2(0.0, 0.0);
+      if (hi >= 0 && hi <= n && hj >= 0 && hj <= n) {
+        const int nd = hj * s + hi;
+        const double2 b0 = rin[nd];
+        const double4 Dr = reinterpret_cast<const double4*>(dinv)[nd];
+        dv = make_double2(k.ith * (Dr.x * b0.x + Dr.y * b0.y), k.ith * (Dr.z * b0.x + Dr.w * b0.y));
+      }
+      sd[0][hy * Gm::HX + hx] = dv;
+    }
+  } else {  // stage d_0 on the tile + M rings (zero outside the domain)
+    for (int idx = t; idx < Gm::HX * Gm::HY; idx += Gm::NT) {
+      const int hi = i0 - M + idx % Gm::HX, hj = j0 - M + idx / Gm::HX;
+      sd[0][idx] = (hi >= 0 && hi <= n && hj >= 0 && hj <= n) ? d0g[hj * s + hi] : make_double2(0.0, 0.0);
+    }
   }
   __syncthreads();
   // steps 1 .. M-1
@@ -1264,30 +1287,29 @@ __global__ void __launch_bounds__(FusedGeom<M>::NT, (FusedGeom<M>::NT <= 256 ? 2
     }
     __syncthreads();
   }
-  // step M (tile only): x += d_{M-1}; r -= A d_{M-1} if wanted
+  // step M (tile only): x += d_{M-1}; r -= A d_{M-1} if pre-smoothing
   if (inside && depth == 0) {
     const double2* din = sd[(M - 1) & 1];
     const double2 dv = din[sidx];
     xa.x += dv.x;
     xa.y += dv.y;
     x[node] = xa;
-    if (want_rM) {
+    if (pre) {
       const double2 y = stencil_apply_reg(interior, Jr, din, sidx, Gm::HX);
       rv.x -= y.x;
       rv.y -= y.y;
-      rout[node] = rv;  // out of place: neighbouring CTAs still read r_0 in their halo
+      rout[node] = rv;
     }
   }
 }
 
 template <int M>
-static void launch_chebM(Ctx& c, const double* dinv, const double* d, const double* r, double* rout, double* x,
+static void launch_chebM(Ctx& c, const double* dinv, const double* rin, const double* d0g, double* rout, double* x,
                          const ChebFCoef& kc, bool pre) {
   using Gm = FusedGeom<M>;
   const dim3 grid((c.n + 1 + Gm::TX - 1) / Gm::TX, (c.n + 1 + kFY - 1) / kFY);
-  k_chebM_stencil<M><<<grid, Gm::NT, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), dinv, (const double2*)d,
-                                                (const double2*)r, (double2*)rout, (double2*)x, kc, pre ? 1 : 0,
-                                                pre ? 1 : 0);
+  k_chebM_stencil<M><<<grid, Gm::NT, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), dinv, (const double2*)rin,
+                                                (const double2*)d0g, (double2*)rout, (double2*)x, kc, pre ? 1 : 0);
 }
 
 // r = b - A x (or r = b if x == NULL); d = Dinv r * c2 (stencil level)
@@ -1504,16 +1526,16 @@ __device__ __forceinline__ double pick(const double v[B], int a) {
 // (its loads are issued before the SpMV loop), and the B x B block-Jacobi product gathers the
 // other components of r with shuffles inside the group.
 
-// y = A x (add = 0) or y += A x (add = 1)
+// y = yin + A x (yin may be NULL: y = A x; yin == y: in place)
 template <int BR, int BC, int G>
 __global__ void __launch_bounds__(256) k_gspmv(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
                                                const double* __restrict__ val, const double* __restrict__ x,
-                                               double* __restrict__ y, int add) {
+                                               const double* yin, double* y) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int row = (int)(t / G), lig = (int)(t % G);
   const bool own = row < nb && lig < BR;
   const long long i = (long long)row * BR + lig;
-  const double y0 = (own && add) ? y[i] : 0.0;
+  const double y0 = (own && yin) ? yin[i] : 0.0;
   double acc[BR];
   grp_row<BR, BC, G>(row, nb, lig, rp, ci, val, x, acc);
   if (own) y[i] = y0 + pick<BR>(acc, lig);
@@ -1767,16 +1789,16 @@ __global__ void __launch_bounds__(512, 1) k_vcycle_tail(const __grid_constant__ 
 }
 
 static void gspmv(Ctx& c, int nb, int br, int bc, long long nnzb, const int* rp, const int* ci, const double* val,
-                  const double* x, double* y, int add) {
+                  const double* x, const double* yin, double* y) {
   const int G = pick_group(nnzb, nb);
   if (br == 3 && bc == 3) {
-    SI_GDISPATCH(G, (k_gspmv<3, 3, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, y, add)))
+    SI_GDISPATCH(G, (k_gspmv<3, 3, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
   } else if (br == 2 && bc == 3) {
-    SI_GDISPATCH(G, (k_gspmv<2, 3, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, y, add)))
+    SI_GDISPATCH(G, (k_gspmv<2, 3, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
   } else if (br == 3 && bc == 2) {
-    SI_GDISPATCH(G, (k_gspmv<3, 2, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, y, add)))
+    SI_GDISPATCH(G, (k_gspmv<3, 2, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
   } else {
-    SI_GDISPATCH(G, (k_gspmv<2, 2, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, y, add)))
+    SI_GDISPATCH(G, (k_gspmv<2, 2, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
   }
   SI_LAUNCHED(c);
 }
@@ -1806,7 +1828,7 @@ static double power_lambda(Ctx& c, Level& L, int lvl) {
     if (lvl == 0 && B == 2)
       stencil_spmv(c, x, y);  // the finest operator is the stencil itself
     else
-      gspmv(c, L.nb, B, B, L.nnzb, L.rp.get(), L.ci.get(), L.valT.get(), x, y, 0);
+      gspmv(c, L.nb, B, B, L.nnzb, L.rp.get(), L.ci.get(), L.valT.get(), x, nullptr, y);
     k_dinv_apply<B><<<grid_for(L.nb), kThreads, 0, c.s>>>(L.nb, L.dinv.get(), y);
     k_sqnorm_part<<<g, kThreads, 0, c.s>>>(N, y, part);
     k_sum_to<<<1, 1024, 0, c.s>>>(part, g, ny2);
@@ -2109,53 +2131,65 @@ static ChebCoef cheb_coef(const Ctx& c, const Level& L) {
 }
 
 // One Chebyshev smoothing on level l for A x = b.  pre: x = 0 start, leaves r = b - A x.
+static int level_degree(const Ctx& c, int l) {
+  return (l == 0 && c.p.cheb_degree0 > 0) ? c.p.cheb_degree0 : c.p.cheb_degree;
+}
+static bool fused_smoother(const Ctx& c, int l) {
+  const int m = level_degree(c, l);
+  return l == 0 && c.p.cheb_fused && m >= 3 && m <= kFMaxM;
+}
+
+// One Chebyshev smoothing on level l for A x = b.  pre: x = 0 start, leaves r = b - A x.
 static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
   Level& L = c.lv[l];
-  const int m = (l == 0 && c.p.cheb_degree0 > 0) ? c.p.cheb_degree0 : c.p.cheb_degree;
+  const int m = level_degree(c, l);
   const ChebCoef k = cheb_coef(c, L);
   double rho = 1.0 / k.sg;
   double* r = L.r.get();
   double* d = L.d.get();
   double* d2 = L.d2.get();
   const bool st = (l == 0);
-  // r = b - A x ; d = Dinv r / th
-  prof_begin(c);
-  if (st) {
-    k_resid_dinv_stencil<<<grid_for(c.Nn), 256, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L.dinv.get(),
-                                                          (const double2*)b, pre ? nullptr : (const double2*)x,
-                                                          (double2*)r, (double2*)d, 1.0 / k.th);
-  } else {
-    const int G = pick_group(L.nnzb, L.nb);
-    SI_GDISPATCH(G, (k_gresid<3, GG><<<ggrid(L.nb, GG), 256, 0, c.s>>>(
-                        L.nb, L.rp.get(), L.ci.get(), L.valT.get(), L.dinv.get(), b, pre ? nullptr : x, r, d,
-                        1.0 / k.th)))
-  }
-  SI_LAUNCHED(c);
-  {
+  const bool fused = fused_smoother(c, l);
+  // r = b - A x ; d = Dinv r / th  (fused pre-smoothing does this inside its launch)
+  if (!(fused && pre)) {
+    prof_begin(c);
+    if (st) {
+      k_resid_dinv_stencil<<<grid_for(c.Nn), 256, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L.dinv.get(),
+                                                            (const double2*)b, pre ? nullptr : (const double2*)x,
+                                                            (double2*)r, (double2*)d, 1.0 / k.th);
+    } else {
+      const int G = pick_group(L.nnzb, L.nb);
+      SI_GDISPATCH(G, (k_gresid<3, GG><<<ggrid(L.nb, GG), 256, 0, c.s>>>(
+                          L.nb, L.rp.get(), L.ci.get(), L.valT.get(), L.dinv.get(), b, pre ? nullptr : x, r, d,
+                          1.0 / k.th)))
+    }
+    SI_LAUNCHED(c);
     const double B = L.b;
     double by = L.nb * (8.0 * B * 3 + 8.0 * B * B);  // b read, r write, d write, dinv
     if (!pre) by += L.nnzb * (8.0 * B * B + (st ? 0.0 : 4.0)) + (st ? 0.0 : 4.0 * (L.nb + 1)) + 8.0 * B * L.nb;
     prof_end(c, st ? PC_RESID0 : PC_RESIDC, by);
   }
-  if (st && m >= 3 && m <= kFMaxM && c.p.cheb_fused) {
+  if (fused) {
     ChebFCoef kc;
+    kc.ith = 1.0 / k.th;
     for (int it = 0; it < m - 1; ++it) {
       const double rho_new = 1.0 / (2.0 * k.sg - rho);
       kc.c1[it] = rho_new * rho;
       kc.c2[it] = 2.0 * rho_new / k.de;
       rho = rho_new;
     }
+    // pre: rin = b, r_m written out of place into L.r; post: rin = r_0, d_0 from d
+    const double* rin = pre ? b : r;
     prof_begin(c);
     switch (m) {
-      case 3: launch_chebM<3>(c, L.dinv.get(), d, r, d2, x, kc, pre); break;
-      case 4: launch_chebM<4>(c, L.dinv.get(), d, r, d2, x, kc, pre); break;
-      case 5: launch_chebM<5>(c, L.dinv.get(), d, r, d2, x, kc, pre); break;
-      default: launch_chebM<6>(c, L.dinv.get(), d, r, d2, x, kc, pre); break;
+      case 3: launch_chebM<3>(c, L.dinv.get(), rin, d, r, x, kc, pre); break;
+      case 4: launch_chebM<4>(c, L.dinv.get(), rin, d, r, x, kc, pre); break;
+      case 5: launch_chebM<5>(c, L.dinv.get(), rin, d, r, x, kc, pre); break;
+      default: launch_chebM<6>(c, L.dinv.get(), rin, d, r, x, kc, pre); break;
     }
     SI_LAUNCHED(c);
-    if (pre) std::swap(L.r, L.d2);  // r_M was written to d2
-    // algorithmic bytes: stencil + Dinv once, d_0 / r_0 / x_0 read, x (and r) written
-    prof_end(c, PC_CHEB0F, (double)c.Nn * (288.0 + 32.0 + 16.0 * 2 + (pre ? 0.0 : 16.0) + 16.0 + (pre ? 16.0 : 0.0)));
+    // algorithmic bytes: stencil + Dinv once, r_0 / b read (+ d_0, x_0 for post), x (+ r_m) written
+    prof_end(c, PC_CHEB0F, (double)c.Nn * (288.0 + 32.0 + 16.0 + (pre ? 32.0 : 48.0)));
     return;
   }
   for (int it = 0; it < m; ++it) {
@@ -2246,12 +2280,12 @@ static void vcycle_level(Ctx& c, int l, const double* b, double* x) {
   Level& Lc = c.lv[l + 1];
   // r_c = R r
   prof_begin(c);
-  gspmv(c, L.nbc, 3, L.b, L.Rnnzb, L.Rrp.get(), L.Rci.get(), L.RvalT.get(), L.r.get(), Lc.rhs.get(), 0);
+  gspmv(c, L.nbc, 3, L.b, L.Rnnzb, L.Rrp.get(), L.Rci.get(), L.RvalT.get(), L.r.get(), nullptr, Lc.rhs.get());
   prof_end(c, PC_TRANSFER, L.Rnnzb * (24.0 * L.b + 4.0) + 4.0 * (L.nbc + 1) + 8.0 * L.b * L.nb + 24.0 * L.nbc);
   vcycle_level(c, l + 1, Lc.rhs.get(), Lc.x.get());
   // x += P e_c
   prof_begin(c);
-  gspmv(c, L.nb, L.b, 3, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.PvalT.get(), Lc.x.get(), x, 1);
+  gspmv(c, L.nb, L.b, 3, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.PvalT.get(), Lc.x.get(), x, x);
   prof_end(c, PC_TRANSFER, L.Pnnzb * (24.0 * L.b + 4.0) + 4.0 * (L.nb + 1) + 16.0 * L.b * L.nb + 24.0 * L.nbc);
   smooth(c, l, b, x, false);
 }

@@ -84,8 +84,6 @@ typedef struct {
   int32_t agg_dist;        /* same on coarse levels */
   int32_t cheb_fused;      /* 1 (default): finest-level Chebyshev(3) as one temporally blocked launch
                               (same arithmetic per node and step); 0: one launch per step */
-  int32_t coarse_tail_dof; /* levels (>= 1) with at most this many DOFs run as one persistent
-                              cooperative launch per V-cycle (same per-row arithmetic); 0: off */
   int32_t cheb_degree0;    /* Chebyshev degree on the finest level (0: cheb_degree) */
 } seaice_params;
 

@@ -8,7 +8,6 @@
 // Everything is deterministic: integer atomics only produce counts/flags, sorting uses
 // CUB's stable radix / segmented sorts, SpGEMM accumulates each output block in a fixed
 // (row-major product) order by a single thread, reductions are fixed-order two-stage.
-#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -18,7 +17,6 @@
 #include "ctx.cuh"
 
 namespace seaice {
-namespace cg = cooperative_groups;
 
 void bsr_apply(Ctx& c, int nb, int br, int bc, const int* rp, const int* ci, const double* val, const double* x,
                double* y);
@@ -188,49 +186,23 @@ __global__ void k_diag_inv(int nb, const int* __restrict__ rp, const int* __rest
   dnorm[r] = sqrt(f2);
 }
 
-// y = Dinv (A x) for BSR A (power iteration).
-template <int B>
-__global__ void k_bsr_spmv_dinv(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
-                                const double* __restrict__ val, const double* __restrict__ dinv,
-                                const double* __restrict__ x, double* __restrict__ y) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= nb) return;
-  double acc[B];
-#pragma unroll
-  for (int a = 0; a < B; ++a) acc[a] = 0.0;
-  for (int e = rp[r]; e < rp[r + 1]; ++e) {
-    const int col = ci[e];
-    const double* v = val + (long long)e * B * B;
-#pragma unroll
-    for (int a = 0; a < B; ++a)
-#pragma unroll
-      for (int b = 0; b < B; ++b) acc[a] += v[a * B + b] * x[(long long)col * B + b];
-  }
-  const double* D = dinv + (long long)r * B * B;
-#pragma unroll
-  for (int a = 0; a < B; ++a) {
-    double s = 0.0;
-#pragma unroll
-    for (int b = 0; b < B; ++b) s += D[a * B + b] * acc[b];
-    y[(long long)r * B + a] = s;
-  }
-}
 
 // y_I = Dinv_I y_I (in place)
 template <int B>
 __global__ void k_dinv_apply(int nb, const double* __restrict__ dinv, double* __restrict__ y) {
+  constexpr int S = (B == 3) ? 4 : B;  // padded coarse vectors (see vstride)
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nb) return;
   double v[B];
 #pragma unroll
-  for (int a = 0; a < B; ++a) v[a] = y[(long long)r * B + a];
+  for (int a = 0; a < B; ++a) v[a] = y[(long long)r * S + a];
   const double* D = dinv + (long long)r * B * B;
 #pragma unroll
   for (int a = 0; a < B; ++a) {
     double s = 0.0;
 #pragma unroll
     for (int b = 0; b < B; ++b) s += D[a * B + b] * v[b];
-    y[(long long)r * B + a] = s;
+    y[(long long)r * S + a] = s;
   }
 }
 
@@ -255,10 +227,18 @@ __global__ void k_scale_rsqrt(long long n, const double* __restrict__ y, const d
   if (i < n) x[i] = y[i] / sqrt(s2[0]);
 }
 
-__global__ void k_power_start(long long N, unsigned long long sl, double* __restrict__ x) {
+// start vector of the power iteration: entry k = B*row + a of the unpadded vector, written at
+// S*row + a of the (possibly padded, S = 4 for B = 3) storage; pads 0
+__global__ void k_power_start(long long N, int B, int S, unsigned long long sl, double* __restrict__ x) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= N) return;
-  const unsigned long long h = splitmix64((unsigned long long)i + sl);
+  const long long row = i / S;
+  const int a = (int)(i - row * S);
+  if (a >= B) {
+    x[i] = 0.0;
+    return;
+  }
+  const unsigned long long h = splitmix64((unsigned long long)(row * B + a) + sl);
   x[i] = 2.0 * ((double)(h >> 11) * 0x1.0p-53) - 1.0;
 }
 
@@ -1109,14 +1089,18 @@ __global__ void k_chol_inverse(int n, const double* __restrict__ Lm, double* __r
 }
 
 // y = M x, dense row-major n x n, warp per row
-__global__ void k_dense_gemv(int n, const double* __restrict__ M, const double* __restrict__ x,
+// y = M x on the coarsest level; DOF k lives at (k / B) * S + k % B of x and y (padded storage)
+__global__ void k_dense_gemv(int n, int B, int S, const double* __restrict__ M, const double* __restrict__ x,
                              double* __restrict__ y) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= n) return;
   double s = 0.0;
-  for (int k = lane; k < n; k += 32) s += M[(long long)w * n + k] * x[k];
+  for (int k = lane; k < n; k += 32) s += M[(long long)w * n + k] * x[(k / B) * S + k % B];
   s = warp_sum(s);
-  if (lane == 0) y[w] = s;
+  if (lane == 0) {
+    y[(w / B) * S + w % B] = s;
+    if (S > B && w % B == B - 1) y[(w / B) * S + B] = 0.0;
+  }
 }
 
 // ------------------------------------------------------------------ smoother kernels
@@ -1347,105 +1331,8 @@ __global__ void __launch_bounds__(256) k_resid_dinv_stencil(int n, int Nn, const
   d[node] = make_double2(c2 * (D.x * rv.x + D.y * rv.y), c2 * (D.z * rv.x + D.w * rv.y));
 }
 
-template <int B>
-__global__ void k_cheb_bsr(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
-                           const double* __restrict__ val, const double* __restrict__ dinv,
-                           const double* __restrict__ d, double* __restrict__ r, double* __restrict__ x,
-                           double* __restrict__ dout, double c1, double c2, int first, int want_r, int want_d) {
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= nb) return;
-  double dv[B];
-#pragma unroll
-  for (int a = 0; a < B; ++a) {
-    dv[a] = d[(long long)row * B + a];
-    const double xv = first ? 0.0 : x[(long long)row * B + a];
-    x[(long long)row * B + a] = xv + dv[a];
-  }
-  if (!want_r) return;
-  double acc[B];
-#pragma unroll
-  for (int a = 0; a < B; ++a) acc[a] = 0.0;
-  for (int e = rp[row]; e < rp[row + 1]; ++e) {
-    const int col = ci[e];
-    const double* v = val + (long long)e * B * B;
-    double xv[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b) xv[b] = __ldg(d + (long long)col * B + b);
-#pragma unroll
-    for (int a = 0; a < B; ++a)
-#pragma unroll
-      for (int b = 0; b < B; ++b) acc[a] += __ldg(v + a * B + b) * xv[b];
-  }
-  double rv[B];
-#pragma unroll
-  for (int a = 0; a < B; ++a) {
-    rv[a] = r[(long long)row * B + a] - acc[a];
-    r[(long long)row * B + a] = rv[a];
-  }
-  if (want_d) {
-    const double* D = dinv + (long long)row * B * B;
-#pragma unroll
-    for (int a = 0; a < B; ++a) {
-      double z = 0.0;
-#pragma unroll
-      for (int b = 0; b < B; ++b) z += D[a * B + b] * rv[b];
-      dout[(long long)row * B + a] = c1 * dv[a] + c2 * z;
-    }
-  }
-}
 
-template <int B>
-__global__ void k_resid_dinv_bsr(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
-                                 const double* __restrict__ val, const double* __restrict__ dinv,
-                                 const double* __restrict__ b, const double* __restrict__ x, double* __restrict__ r,
-                                 double* __restrict__ d, double c2) {
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= nb) return;
-  double rv[B];
-#pragma unroll
-  for (int a = 0; a < B; ++a) rv[a] = b[(long long)row * B + a];
-  if (x) {
-    for (int e = rp[row]; e < rp[row + 1]; ++e) {
-      const int col = ci[e];
-      const double* v = val + (long long)e * B * B;
-#pragma unroll
-      for (int a = 0; a < B; ++a)
-#pragma unroll
-        for (int bb = 0; bb < B; ++bb) rv[a] -= v[a * B + bb] * x[(long long)col * B + bb];
-    }
-  }
-  const double* D = dinv + (long long)row * B * B;
-#pragma unroll
-  for (int a = 0; a < B; ++a) r[(long long)row * B + a] = rv[a];
-#pragma unroll
-  for (int a = 0; a < B; ++a) {
-    double z = 0.0;
-#pragma unroll
-    for (int bb = 0; bb < B; ++bb) z += D[a * B + bb] * rv[bb];
-    d[(long long)row * B + a] = c2 * z;
-  }
-}
 
-// y += X x (BSR, accumulate) — prolongation
-template <int BR, int BC>
-__global__ void k_bsr_spmv_add(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
-                               const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= nb) return;
-  double acc[BR];
-#pragma unroll
-  for (int a = 0; a < BR; ++a) acc[a] = y[(long long)r * BR + a];
-  for (int e = rp[r]; e < rp[r + 1]; ++e) {
-    const int col = ci[e];
-    const double* v = val + (long long)e * BR * BC;
-#pragma unroll
-    for (int a = 0; a < BR; ++a)
-#pragma unroll
-      for (int b = 0; b < BC; ++b) acc[a] += v[a * BC + b] * __ldg(x + (long long)col * BC + b);
-  }
-#pragma unroll
-  for (int a = 0; a < BR; ++a) y[(long long)r * BR + a] = acc[a];
-}
 
 // ------------------------------------------------------------------ group-per-row BSR kernels
 // V-cycle copy of a block array in the chunk-of-32 SoA layout (Level::valT): a group's lanes
@@ -1465,6 +1352,24 @@ static void tile_copy(Ctx& c, DBuf<double>& out, const double* val, long long nn
   SI_LAUNCHED(c);
 }
 
+// Coarse-level vectors (b = 3) are stored padded to 4 doubles per block row (32-byte aligned;
+// the pad is kept 0), so the x gather of a 3x3 block is ONE 256-bit load instead of three
+// 8-byte loads (the group kernels are L1-wavefront bound).  Level 0 (b = 2) is unpadded.
+__host__ __device__ constexpr int vstride(int B) { return B == 3 ? 4 : B; }
+
+template <int BC>
+__device__ __forceinline__ void load_xblk(const double* __restrict__ x, int col, double xv[BC]) {
+  if constexpr (BC == 3) {
+    const double* p = x + (long long)col * 4;
+    double w;
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(xv[0]), "=d"(xv[1]), "=d"(xv[2]), "=d"(w) : "l"(p));
+  } else {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(x) + col);
+    xv[0] = v.x;
+    xv[1] = v.y;
+  }
+}
+
 // G consecutive lanes own one block row: lane l reads blocks e = rp[row] + l, + G, ...
 // so the G blocks a group touches per step are contiguous in memory (coalesced), and the
 // BR partial sums are combined with an xor-butterfly (same order on every lane).  The loop is
@@ -1478,7 +1383,6 @@ __device__ __forceinline__ void blk_fma(const double* __restrict__ val, int e, c
     for (int b = 0; b < BC; ++b) acc[a] += __ldg(v + (a * BC + b) * 32) * xv[b];
 }
 
-constexpr bool kUnroll2 = true;
 template <int BR, int BC, int G>
 __device__ __forceinline__ void grp_row(int row, int nb, int lig, const int* __restrict__ rp,
                                         const int* __restrict__ ci, const double* __restrict__ val,
@@ -1488,22 +1392,17 @@ __device__ __forceinline__ void grp_row(int row, int nb, int lig, const int* __r
   if (row < nb) {
     const int e1 = __ldg(rp + row + 1);
     int e = __ldg(rp + row) + lig;
-    for (; kUnroll2 && e + G < e1; e += 2 * G) {
+    for (; e + G < e1; e += 2 * G) {
       const int c0 = __ldg(ci + e), c1 = __ldg(ci + e + G);
       double x0[BC], x1[BC];
-#pragma unroll
-      for (int b = 0; b < BC; ++b) {
-        x0[b] = __ldg(x + (long long)c0 * BC + b);
-        x1[b] = __ldg(x + (long long)c1 * BC + b);
-      }
+      load_xblk<BC>(x, c0, x0);
+      load_xblk<BC>(x, c1, x1);
       blk_fma<BR, BC>(val, e, x0, acc);
       blk_fma<BR, BC>(val, e + G, x1, acc);
     }
     for (; e < e1; e += G) {
-      const int c0 = __ldg(ci + e);
       double x0[BC];
-#pragma unroll
-      for (int b = 0; b < BC; ++b) x0[b] = __ldg(x + (long long)c0 * BC + b);
+      load_xblk<BC>(x, __ldg(ci + e), x0);
       blk_fma<BR, BC>(val, e, x0, acc);
     }
   }
@@ -1522,32 +1421,32 @@ __device__ __forceinline__ double pick(const double v[B], int a) {
   return r;
 }
 
-// The row epilogues are spread over the group: lane a < B owns component a of the block row
-// (its loads are issued before the SpMV loop), and the B x B block-Jacobi product gathers the
-// other components of r with shuffles inside the group.
-
-// y = yin + A x (yin may be NULL: y = A x; yin == y: in place)
+// y = yin + A x (yin may be NULL: y = A x; yin == y: in place).  Lane a < BR of a group owns
+// component a of the block row; lane BR writes the pad (0) of a padded row.
 template <int BR, int BC, int G>
 __global__ void __launch_bounds__(256) k_gspmv(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
                                                const double* __restrict__ val, const double* __restrict__ x,
                                                const double* yin, double* y) {
+  constexpr int SR = vstride(BR);
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int row = (int)(t / G), lig = (int)(t % G);
   const bool own = row < nb && lig < BR;
-  const long long i = (long long)row * BR + lig;
+  const long long i = (long long)row * SR + lig;
   const double y0 = (own && yin) ? yin[i] : 0.0;
   double acc[BR];
   grp_row<BR, BC, G>(row, nb, lig, rp, ci, val, x, acc);
   if (own) y[i] = y0 + pick<BR>(acc, lig);
+  else if (SR > BR && row < nb && lig == BR) y[i] = 0.0;
 }
 
-// fused Chebyshev step (same semantics as k_cheb_stencil) on a coarse level
+// fused Chebyshev step (same semantics as k_cheb_stencil) on a coarse level (padded vectors)
 template <int B, int G>
 __global__ void __launch_bounds__(256) k_gcheb(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
                                                const double* __restrict__ val, const double* __restrict__ dinv,
                                                const double* __restrict__ d, double* __restrict__ r,
                                                double* __restrict__ x, double* __restrict__ dout, double c1,
                                                double c2, int first, int want_r, int want_d) {
+  constexpr int S = vstride(B);
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int row = (int)(t / G), lig = (int)(t % G);
   double acc[B];
@@ -1556,15 +1455,16 @@ __global__ void __launch_bounds__(256) k_gcheb(int nb, const int* __restrict__ r
   double dv[B];
 #pragma unroll
   for (int a = 0; a < B; ++a) {
-    const long long i = (long long)row * B + a;
+    const long long i = (long long)row * S + a;
     dv[a] = d[i];
     x[i] = (first ? 0.0 : x[i]) + dv[a];
   }
+  if (S > B && first) x[(long long)row * S + B] = 0.0;
   if (!want_r) return;
   double rv[B];
 #pragma unroll
   for (int a = 0; a < B; ++a) {
-    const long long i = (long long)row * B + a;
+    const long long i = (long long)row * S + a;
     rv[a] = r[i] - acc[a];
     r[i] = rv[a];
   }
@@ -1575,21 +1475,23 @@ __global__ void __launch_bounds__(256) k_gcheb(int nb, const int* __restrict__ r
       double z = 0.0;
 #pragma unroll
       for (int b = 0; b < B; ++b) z += D[a * B + b] * rv[b];
-      dout[(long long)row * B + a] = c1 * dv[a] + c2 * z;
+      dout[(long long)row * S + a] = c1 * dv[a] + c2 * z;
     }
+    if (S > B) dout[(long long)row * S + B] = 0.0;
   }
 }
 
-// r = b - A x (x may be NULL: r = b); d = c2 Dinv r
+// r = b - A x (x may be NULL: r = b); d = c2 Dinv r (padded vectors)
 template <int B, int G>
 __global__ void __launch_bounds__(256) k_gresid(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
                                                 const double* __restrict__ val, const double* __restrict__ dinv,
                                                 const double* __restrict__ b, const double* __restrict__ x,
                                                 double* __restrict__ r, double* __restrict__ d, double c2) {
+  constexpr int S = vstride(B);
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int row = (int)(t / G), lig = (int)(t % G);
   const bool own = row < nb && lig < B;
-  const long long i = (long long)row * B + lig;
+  const long long i = (long long)row * S + lig;
   double bo = 0.0, D[B];
 #pragma unroll
   for (int k = 0; k < B; ++k) D[k] = 0.0;
@@ -1610,6 +1512,10 @@ __global__ void __launch_bounds__(256) k_gresid(int nb, const int* __restrict__ 
 #pragma unroll
   for (int k = 0; k < B; ++k) z += D[k] * __shfl_sync(0xffffffffu, rv, k, G);
   if (own) d[i] = c2 * z;
+  else if (S > B && row < nb && lig == B) {
+    r[i] = 0.0;
+    d[i] = 0.0;
+  }
 }
 
 static int pick_group(long long nnzb, int nb) {
@@ -1629,164 +1535,6 @@ static int ggrid(int nb, int G) { return (int)(((long long)nb * G + 255) / 256);
     case 16: { constexpr int GG = 16; CALL; } break; \
     default: { constexpr int GG = 32; CALL; } break; \
   }
-
-// ------------------------------------------------------------------ coarse tail (persistent)
-// The small coarse levels (A resident in L2) cost one launch latency per kernel, ~10 kernels
-// per level and V-cycle.  Below Ctx::tail_start the whole V-cycle (pre-smoothing, restriction,
-// dense coarsest solve, prolongation, post-smoothing) runs in ONE cooperative launch with a
-// grid-wide barrier between dependent phases; each phase is the same per-row arithmetic as
-// the corresponding k_gresid / k_gcheb / k_gspmv launch (same group size, same order).
-constexpr int kTailMaxLev = 10, kTailMaxDeg = 8;
-struct TailLevel {
-  int nb, nbc, GA, GR, GP;
-  const int *rp, *ci, *Rrp, *Rci, *Prp, *Pci;
-  const double *valT, *dinv, *RvalT, *PvalT;
-  double *x, *rhs, *r, *d, *d2;
-  double ith;                                 // 1 / theta
-  double c1[kTailMaxDeg], c2[kTailMaxDeg];    // Chebyshev step coefficients
-};
-struct TailArgs {
-  int nl, m, cn;
-  const double* cinv;
-  TailLevel L[kTailMaxLev];
-};
-
-template <int G>
-__device__ __forceinline__ void tail_resid(const TailLevel& L, const double* __restrict__ b,
-                                           const double* __restrict__ x, long long gt, long long gs) {
-  const long long tot = ((long long)L.nb * G + 31) / 32 * 32;
-  for (long long tt = gt; tt < tot; tt += gs) {
-    const int row = (int)(tt / G), lig = (int)(tt % G);
-    const bool own = row < L.nb && lig < 3;
-    const long long i = (long long)row * 3 + lig;
-    double bo = 0.0, D[3] = {0.0, 0.0, 0.0};
-    if (own) {
-      bo = b[i];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) D[k] = L.dinv[(long long)row * 9 + lig * 3 + k];
-    }
-    double acc[3];
-    if (x) grp_row<3, 3, G>(row, L.nb, lig, L.rp, L.ci, L.valT, x, acc);
-    else acc[0] = acc[1] = acc[2] = 0.0;
-    const double rv = bo - (own ? pick<3>(acc, lig) : 0.0);
-    if (own) L.r[i] = rv;
-    double z = 0.0;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) z += D[k] * __shfl_sync(0xffffffffu, rv, k, G);
-    if (own) L.d[i] = L.ith * z;
-  }
-}
-
-template <int G>
-__device__ __forceinline__ void tail_cheb(const TailLevel& L, const double* __restrict__ d,
-                                          double* __restrict__ dout, double c1, double c2, int first, int want_r,
-                                          int want_d, long long gt, long long gs) {
-  const long long tot = ((long long)L.nb * G + 31) / 32 * 32;
-  for (long long tt = gt; tt < tot; tt += gs) {
-    const int row = (int)(tt / G), lig = (int)(tt % G);
-    double acc[3];
-    if (want_r) grp_row<3, 3, G>(row, L.nb, lig, L.rp, L.ci, L.valT, d, acc);
-    if (row >= L.nb || lig != 0) continue;
-    double dv[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const long long i = (long long)row * 3 + a;
-      dv[a] = d[i];
-      L.x[i] = (first ? 0.0 : L.x[i]) + dv[a];
-    }
-    if (!want_r) continue;
-    double rv[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const long long i = (long long)row * 3 + a;
-      rv[a] = L.r[i] - acc[a];
-      L.r[i] = rv[a];
-    }
-    if (want_d) {
-      const double* D = L.dinv + (long long)row * 9;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        double z = 0.0;
-#pragma unroll
-        for (int b = 0; b < 3; ++b) z += D[a * 3 + b] * rv[b];
-        dout[(long long)row * 3 + a] = c1 * dv[a] + c2 * z;
-      }
-    }
-  }
-}
-
-template <int G>
-__device__ __forceinline__ void tail_spmv(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
-                                          const double* __restrict__ val, const double* __restrict__ x,
-                                          double* __restrict__ y, int add, long long gt, long long gs) {
-  const long long tot = ((long long)nb * G + 31) / 32 * 32;
-  for (long long tt = gt; tt < tot; tt += gs) {
-    const int row = (int)(tt / G), lig = (int)(tt % G);
-    const bool own = row < nb && lig < 3;
-    const long long i = (long long)row * 3 + lig;
-    const double y0 = (own && add) ? y[i] : 0.0;
-    double acc[3];
-    grp_row<3, 3, G>(row, nb, lig, rp, ci, val, x, acc);
-    if (own) y[i] = y0 + pick<3>(acc, lig);
-  }
-}
-
-#define SI_TDISPATCH(G, CALL) \
-  switch (G) {                \
-    case 4: { constexpr int GG = 4; CALL; } break;   \
-    case 8: { constexpr int GG = 8; CALL; } break;   \
-    case 16: { constexpr int GG = 16; CALL; } break; \
-    default: { constexpr int GG = 32; CALL; } break; \
-  }
-
-__global__ void __launch_bounds__(512, 1) k_vcycle_tail(const __grid_constant__ TailArgs A) {
-  cg::grid_group grid = cg::this_grid();
-  const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long gs = (long long)gridDim.x * blockDim.x;
-  const int nl = A.nl, m = A.m;
-  for (int l = 0; l < nl - 1; ++l) {  // down: pre-smoothing from x = 0, restriction
-    const TailLevel& L = A.L[l];
-    SI_TDISPATCH(L.GA, (tail_resid<GG>(L, L.rhs, nullptr, gt, gs)));
-    grid.sync();
-    double* d = L.d;
-    double* d2 = L.d2;
-    for (int it = 0; it < m; ++it) {
-      const int want_d = (it < m - 1) ? 1 : 0;
-      SI_TDISPATCH(L.GA, (tail_cheb<GG>(L, d, d2, L.c1[it], L.c2[it], it == 0 ? 1 : 0, 1, want_d, gt, gs)));
-      grid.sync();
-      double* tp = d; d = d2; d2 = tp;
-    }
-    SI_TDISPATCH(L.GR, (tail_spmv<GG>(L.nbc, L.Rrp, L.Rci, L.RvalT, L.r, A.L[l + 1].rhs, 0, gt, gs)));
-    grid.sync();
-  }
-  {  // dense coarsest solve x = C^-1 b (warp per row)
-    const TailLevel& Lc = A.L[nl - 1];
-    const long long nw = gs >> 5;
-    const int lane = threadIdx.x & 31;
-    for (long long w = gt >> 5; w < A.cn; w += nw) {
-      double sacc = 0.0;
-      for (int k = lane; k < A.cn; k += 32) sacc += A.cinv[w * A.cn + k] * Lc.rhs[k];
-      sacc = warp_sum(sacc);
-      if (lane == 0) Lc.x[w] = sacc;
-    }
-    grid.sync();
-  }
-  for (int l = nl - 2; l >= 0; --l) {  // up: prolongation, post-smoothing
-    const TailLevel& L = A.L[l];
-    SI_TDISPATCH(L.GP, (tail_spmv<GG>(L.nb, L.Prp, L.Pci, L.PvalT, A.L[l + 1].x, L.x, 1, gt, gs)));
-    grid.sync();
-    SI_TDISPATCH(L.GA, (tail_resid<GG>(L, L.rhs, L.x, gt, gs)));
-    grid.sync();
-    double* d = L.d;
-    double* d2 = L.d2;
-    for (int it = 0; it < m; ++it) {
-      const int last = (it == m - 1) ? 1 : 0;
-      SI_TDISPATCH(L.GA, (tail_cheb<GG>(L, d, d2, L.c1[it], L.c2[it], 0, !last, !last, gt, gs)));
-      grid.sync();
-      double* tp = d; d = d2; d2 = tp;
-    }
-  }
-}
 
 static void gspmv(Ctx& c, int nb, int br, int bc, long long nnzb, const int* rp, const int* ci, const double* val,
                   const double* x, const double* yin, double* y) {
@@ -1808,11 +1556,11 @@ static BsrMat view(Level& L) { return BsrMat{L.nb, L.nb, L.b, L.b, L.nnzb, L.rp.
 
 template <int B>
 static double power_lambda(Ctx& c, Level& L, int lvl) {
-  const long long N = (long long)L.nb * B;
+  const long long N = (long long)L.nb * vstride(B);  // storage length (pads stay 0)
   Scratch S(c);
   double* x = S.get<double>(N);
   double* y = S.get<double>(N);
-  k_power_start<<<grid_for(N), kThreads, 0, c.s>>>(N, salt(c.p.amg_seed, lvl, 7), x);
+  k_power_start<<<grid_for(N), kThreads, 0, c.s>>>(N, B, vstride(B), salt(c.p.amg_seed, lvl, 7), x);
   SI_LAUNCHED(c);
   // normalisation stays on the device (no host round trip per iteration); lambda is
   // ||D^-1 A x|| of the last unit-norm iterate
@@ -2071,8 +1819,12 @@ void amg_setup_impl(Ctx& c) {
     tick(c, "power", lvl);
     nnz_total += L.nnzb * L.b * L.b;
     const long long ndof = (long long)L.nb * L.b;
-    // work vectors for the V-cycle
-    for (auto* v : {&L.x, &L.rhs, &L.r, &L.d, &L.d2, &L.z}) v->ensure(c.al, ndof);
+    // work vectors for the V-cycle (coarse levels padded to 4 per block row, pads 0)
+    const long long nst = (long long)L.nb * vstride(L.b);
+    for (auto* v : {&L.x, &L.rhs, &L.r, &L.d, &L.d2, &L.z}) {
+      v->ensure(c.al, nst);
+      if (L.b == 3) SI_CUDA(cudaMemsetAsync(v->get(), 0, sizeof(double) * nst, c.s));
+    }
     const bool last_allowed = (lvl + 1 >= c.p.max_levels);
     if (ndof <= c.p.coarse_max_dof || last_allowed) break;
     const int na = (L.b == 2) ? aggregate_level<2>(c, L, lvl, dnorm, S) : aggregate_level<3>(c, L, lvl, dnorm, S);
@@ -2097,23 +1849,6 @@ void amg_setup_impl(Ctx& c) {
   SI_CHECK(!(flag & 4), SEAICE_ENONFINITE, "AMG: singular diagonal block");
   SI_CHECK(!(flag & 8), SEAICE_ENONFINITE, "AMG: coarse matrix not positive definite");
   c.op_complexity = (double)nnz_total / (double)nnz0;
-  // persistent coarse tail: the levels >= tail_start (all b = 3, DOFs <= coarse_tail_dof)
-  c.tail_start = 0;
-  if (c.p.coarse_tail_dof > 0 && c.p.cheb_degree <= kTailMaxDeg) {
-    for (int l = 1; l < c.nlev; ++l) {
-      if ((long long)c.lv[l].nb * c.lv[l].b <= c.p.coarse_tail_dof) {
-        if (c.nlev - l <= kTailMaxLev && l < c.nlev - 1) c.tail_start = l;
-        break;
-      }
-    }
-  }
-  if (c.tail_start > 0 && c.tail_grid == 0) {
-    int dev = 0, sms = 0, per = 0;
-    SI_CUDA(cudaGetDevice(&dev));
-    SI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    SI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_vcycle_tail, 512, 0));
-    c.tail_grid = sms * (per < 1 ? 1 : per);
-  }
   c.amg_ready = true;
 }
 
@@ -2223,55 +1958,11 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
   }
 }
 
-static void vcycle_tail(Ctx& c) {
-  const int l0 = c.tail_start;
-  TailArgs A;
-  A.nl = c.nlev - l0;
-  A.m = c.p.cheb_degree;
-  A.cn = c.cn;
-  A.cinv = c.cinv.get();
-  double bytes = 8.0 * c.cn * c.cn;
-  for (int k = 0; k < A.nl; ++k) {
-    Level& L = c.lv[l0 + k];
-    TailLevel& T = A.L[k];
-    T.nb = L.nb;
-    T.nbc = L.nbc;
-    T.GA = pick_group(L.nnzb, L.nb);
-    T.GR = pick_group(L.Rnnzb, L.nbc);
-    T.GP = pick_group(L.Pnnzb, L.nb);
-    T.rp = L.rp.get(); T.ci = L.ci.get(); T.valT = L.valT.get(); T.dinv = L.dinv.get();
-    T.Rrp = L.Rrp.get(); T.Rci = L.Rci.get(); T.RvalT = L.RvalT.get();
-    T.Prp = L.Prp.get(); T.Pci = L.Pci.get(); T.PvalT = L.PvalT.get();
-    T.x = L.x.get(); T.rhs = L.rhs.get(); T.r = L.r.get(); T.d = L.d.get(); T.d2 = L.d2.get();
-    if (k == A.nl - 1) break;  // coarsest: dense solve only
-    const ChebCoef kc = cheb_coef(c, L);
-    T.ith = 1.0 / kc.th;
-    double rho = 1.0 / kc.sg;
-    for (int it = 0; it < A.m; ++it) {
-      const double rho_new = 1.0 / (2.0 * kc.sg - rho);
-      T.c1[it] = rho_new * rho;
-      T.c2[it] = 2.0 * rho_new / kc.de;
-      rho = rho_new;
-    }
-    // A read (2m + 1) times, R and P once, ~10 vector passes
-    bytes += (2.0 * A.m + 1.0) * L.nnzb * 76.0 + (L.Rnnzb + L.Pnnzb) * 76.0 + 10.0 * 24.0 * L.nb;
-  }
-  prof_begin(c);
-  void* args[] = {(void*)&A};
-  SI_CUDA(cudaLaunchCooperativeKernel((const void*)k_vcycle_tail, dim3(c.tail_grid), dim3(512), args, 0, c.s));
-  SI_LAUNCHED(c);
-  prof_end(c, PC_TAIL, bytes);
-}
-
 static void vcycle_level(Ctx& c, int l, const double* b, double* x) {
   Level& L = c.lv[l];
-  if (l > 0 && l == c.tail_start) {  // b = L.rhs, x = L.x
-    vcycle_tail(c);
-    return;
-  }
   if (l + 1 == c.nlev) {
     prof_begin(c);
-    k_dense_gemv<<<grid_for((long long)c.cn * 32, 256), 256, 0, c.s>>>(c.cn, c.cinv.get(), b, x);
+    k_dense_gemv<<<grid_for((long long)c.cn * 32, 256), 256, 0, c.s>>>(c.cn, L.b, vstride(L.b), c.cinv.get(), b, x);
     SI_LAUNCHED(c);
     prof_end(c, PC_COARSE, 8.0 * c.cn * c.cn + 16.0 * c.cn);
     return;

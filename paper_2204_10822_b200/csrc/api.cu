@@ -65,7 +65,6 @@ void validate(const seaice_params* p) {
   SI_CHECK((p->agg_dist0 == 1 || p->agg_dist0 == 2) && (p->agg_dist == 1 || p->agg_dist == 2), SEAICE_EINVAL,
            "agg_dist0/agg_dist must be 1 or 2");
   SI_CHECK(p->cheb_fused == 0 || p->cheb_fused == 1, SEAICE_EINVAL, "cheb_fused must be 0 or 1");
-  SI_CHECK(p->coarse_tail_dof >= 0, SEAICE_EINVAL, "coarse_tail_dof must be >= 0");
   SI_CHECK(p->cheb_degree0 >= 0 && p->cheb_degree0 <= 16, SEAICE_EINVAL, "cheb_degree0 in [0,16]");
 }
 
@@ -229,7 +228,6 @@ void seaice_default_params(seaice_params* p, int32_t n) {
   p->agg_dist0 = 2;
   p->agg_dist = 2;
   p->cheb_fused = 1;
-  p->coarse_tail_dof = 0;
   p->cheb_degree0 = 0;  // measured no gain on B200 (grid barriers ~ launch gaps in the graph)
 }
 

@@ -96,7 +96,6 @@ enum ProfClass {
   PC_RESIDC = 11,   // residual + Dinv, coarse levels
   PC_PIUPD = 12,    // K12 dual update
   PC_CHEB0F = 13,   // K4 three Chebyshev steps fused (temporal blocking), finest level
-  PC_TAIL = 14,     // K4-K6 persistent V-cycle over the small coarse levels
   PC_NCLASS = 16
 };
 struct Prof {
@@ -168,8 +167,6 @@ struct Ctx {
   DBuf<double> vc_in, vc_out;
   DBuf<double> cinv;  // dense coarse inverse
   int cn = 0;         // coarse DOFs
-  int tail_start = 0; // first level of the persistent coarse tail (0: none)
-  int tail_grid = 0;  // co-resident CTAs of k_vcycle_tail
   double op_complexity = 0.0;
   DBuf<int> iwork;
   DBuf<double> dwork;

@@ -34,7 +34,7 @@ class Params(C.Structure):
                 ("cheb_degree", C.c_int32), ("coarse_max_dof", C.c_int32), ("max_levels", C.c_int32),
                 ("cheb_lower", C.c_double), ("cheb_upper", C.c_double), ("power_iters", C.c_int32),
                 ("project_pi", C.c_int32), ("amg_seed", C.c_uint64), ("agg_dist0", C.c_int32),
-                ("agg_dist", C.c_int32), ("cheb_fused", C.c_int32), ("coarse_tail_dof", C.c_int32),
+                ("agg_dist", C.c_int32), ("cheb_fused", C.c_int32),
                 ("cheb_degree0", C.c_int32)]
 
 
@@ -259,7 +259,7 @@ class SeaIce:
         return int(self.L.seaice_launch_count(self.h))
 
     PROF_NAMES = ["assemble", "spmv0", "cheb0", "cheb_coarse", "resid0", "multidot", "maxpy_norm", "maxpy",
-                  "delta_energy", "transfer", "coarse_solve", "resid_coarse", "pi_update", "cheb0_fused", "coarse_tail"]
+                  "delta_energy", "transfer", "coarse_solve", "resid_coarse", "pi_update", "cheb0_fused"]
 
     def profile(self, on: bool):
         self._check(self.L.seaice_profile_enable(self.h, 1 if on else 0))

@@ -211,21 +211,3 @@ def test_fused_chebyshev_matches_per_step(n):
         out.append(np_(ctx.precond_apply(r)))
     assert np.linalg.norm(out[1] - out[0]) <= 1e-12 * np.linalg.norm(out[0])
 
-
-def test_coarse_tail_matches_per_level_launches():
-    """The persistent cooperative coarse tail (coarse_tail_dof > 0) runs the same per-row
-    arithmetic as the per-level launches: V-cycles agree to rounding."""
-    n = 48
-    inp, pb, v, pi = newton_state(n, 4, 0)
-    v = wl.random_velocity(n, 7, amp=0.05)
-    pi = wl.random_pi(n, 8, max_norm=1.2)
-    out = []
-    for tail in (0, 100000):
-        ctx = make_ctx(n, coarse_tail_dof=tail)
-        ctx.set_inputs(inp)
-        ctx.assemble_jacobian(v, pi.ravel(), want_csr=False)
-        nlev, _ = ctx.amg_setup()
-        assert nlev >= 3
-        r = wl.random_interior_vector(n, 9)
-        out.append(np_(ctx.precond_apply(r)))
-    assert np.linalg.norm(out[1] - out[0]) <= 1e-12 * np.linalg.norm(out[0])

@@ -1523,6 +1523,9 @@ static int pick_group(long long nnzb, int nb) {
   const double avg = nb > 0 ? (double)nnzb / nb : 1.0;
   // measured on B200 (scripts/vcycle_bench.py): ~2-4 blocks per lane is the sweet spot
   int g = avg <= 14.0 ? 4 : avg <= 40.0 ? 8 : avg <= 120.0 ? 16 : 32;
+  // small levels cannot fill the GPU anyway: a full warp per row shortens each row's chain of
+  // dependent (column index -> x gather) loads, which is what these launches wait on
+  if ((long long)nb * 32 <= 148LL * 2048) g = 32;
   g = shift >= 0 ? (g << shift) : (g >> -shift);
   return g < 4 ? 4 : (g > 32 ? 32 : g);
 }

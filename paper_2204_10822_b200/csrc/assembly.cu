@@ -977,6 +977,467 @@ __global__ void __launch_bounds__(kTThreads, 2) k_assemble_modal(Phys ph, ElemK 
   if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = bs;
 }
 
+// ------------------------------------------------------------------ K1, Hadamard element algebra
+// Same tiling and shared-memory layout as k_assemble_modal; the per-cell arithmetic is cut
+// further with the 4-point Walsh-Hadamard structure of the uniform Q1 cell (exact identities):
+//  * Phi = [phi_a] (rows phi_a = (1, xi_a, eta_a, xi_a eta_a)) is a signed Hadamard matrix, so a
+//    nodal field f has modal coefficients F^ = Phi^T f (one 8-add butterfly) and
+//      f(q) = (F0 + xi_q F1 + eta_q F2 + xi_q eta_q F3)/4,  df/dx = (F1 + eta F3)/(2dx),
+//      df/dy = (F2 + xi F3)/(2dx):  tau^(v)(q) is affine in (xi_q, eta_q) with 7 coefficients.
+//  * The per-Gauss-point Q_ij and drag values are parked (9 per q) and reduced to their four
+//    q-moments (sum, xi-, eta-, xi*eta-weighted) by the same butterfly.
+//  * Each 4x4 component block of the element matrix is E^km = Phi M^km Phi^T with
+//      M^km = (1/16) sum_q E_km(q) m_q m_q^T  (mass + ocean drag, m_q = (1, xi_q, eta_q, xi_q eta_q))
+//             + [0, 0; 0, S^km]                (viscous stiffness, S of k_assemble_modal),
+//    i.e. one 2-D 4x4 Walsh-Hadamard transform per block instead of a per-entry expansion.
+//  * The element residual stays in per-Gauss-point nodal form (it decides Newton convergence at
+//    1e-8, see k_assemble_modal), with the factors -w, dt, 1/dx folded into 5 per-q coefficients.
+struct ElemH {
+  double ka, kb;              // al/(2dx), be/(2dx): tau^ coefficients from unscaled modal gradients
+  double al, be;              // 1/sqrt2, 1/(sqrt2 e)
+  double ka1, ka2, ka3;       // a_i = p_i . pi^ in terms of (p11, p12, p22)
+  double sc;                  // w dt / (2dx)^2
+  double pp11, pp13, pp22;    // p_i . p_j
+  double mwdtdx;              // -w dt / dx
+  double hwdtdx;              // w dt / (2 dx)
+  double wdtco;               // w dt C_o rho_o
+  double kd;                  // w dt C_o rho_o / 16 (drag block of M^)
+  double mass16;              // 4 w / 16 (times rho_i h: consistent mass in M^00)
+  double w, dmin2;
+};
+static ElemH make_elemh(const Phys& ph) {
+  ElemH k;
+  const double inv_dx = 1.0 / ph.dx;
+  k.al = kR2I;
+  k.be = kR2I / ph.e;
+  k.ka = 0.5 * inv_dx * k.al;
+  k.kb = 0.5 * inv_dx * k.be;
+  k.ka1 = (k.al + k.be) * kR2I;
+  k.ka3 = (k.al - k.be) * kR2I;
+  k.ka2 = kR2 * k.be;
+  k.w = 0.25 * ph.dx * ph.dx;
+  const double wdt = k.w * ph.dt;
+  k.sc = wdt * 0.25 * inv_dx * inv_dx;
+  k.pp11 = k.al * k.al + k.be * k.be;
+  k.pp13 = k.al * k.al - k.be * k.be;
+  k.pp22 = k.be * k.be;
+  k.mwdtdx = -wdt * inv_dx;
+  k.hwdtdx = 0.5 * wdt * inv_dx;
+  k.wdtco = wdt * ph.C_o * ph.rho_o;
+  k.kd = k.wdtco / 16.0;
+  k.mass16 = 4.0 * k.w / 16.0;
+  k.dmin2 = ph.delta_min * ph.delta_min;
+  return k;
+}
+
+// Per-Gauss-point constants (q order (-g,-g), (g,-g), (g,g), (-g,g)); uniform across a warp.
+struct QC {
+  double xq, eq, x4, e4, xe4;   // xi_q, eta_q, xi_q/4, eta_q/4, xi_q eta_q/4
+  double N[4], Gx[4], Gy[4];    // N_a(q), dx * dN_a/dx(q), dx * dN_a/dy(q)
+};
+__constant__ QC cQ[4];
+static void upload_qc() {
+  static bool done = false;
+  if (done) return;
+  QC h[4];
+  for (int q = 0; q < 4; ++q) {
+    h[q].xq = xi_q(q);
+    h[q].eq = eta_q(q);
+    h[q].x4 = 0.25 * xi_q(q);
+    h[q].e4 = 0.25 * eta_q(q);
+    h[q].xe4 = 0.25 * xi_q(q) * eta_q(q);
+    for (int a = 0; a < 4; ++a) {
+      h[q].N[a] = Nq(q, a);
+      h[q].Gx[a] = Gx(q, a);
+      h[q].Gy[a] = Gy(q, a);
+    }
+  }
+  SI_CUDA(cudaMemcpyToSymbol(cQ, h, sizeof(h)));
+  done = true;
+}
+
+// F^ = Phi^T f: (f0+f1+f2+f3, -f0+f1+f2-f3, -f0-f1+f2+f3, f0-f1+f2-f3)
+__device__ __forceinline__ void had_t(double f0, double f1, double f2, double f3, double F[4]) {
+  const double s02 = f0 + f2, d02 = f2 - f0, s13 = f1 + f3, d13 = f1 - f3;
+  F[0] = s02 + s13;
+  F[1] = d02 + d13;
+  F[2] = d02 - d13;
+  F[3] = s02 - s13;
+}
+// y_a = phi_a . r for a = 0..3 (phi_0 = (1,-1,-1,1), phi_1 = (1,1,-1,-1), phi_2 = 1, phi_3 = (1,-1,1,-1))
+__device__ __forceinline__ void had_n(double r0, double r1, double r2, double r3, double y[4]) {
+  const double s03 = r0 + r3, d03 = r0 - r3, s12 = r1 + r2, d12 = r1 - r2;
+  y[0] = s03 - s12;
+  y[1] = d03 + d12;
+  y[2] = s03 + s12;
+  y[3] = d03 - d12;
+}
+// E = Phi M Phi^T for a 4x4 M (row-major); SYM: M symmetric, only a <= b of E is used.
+template <bool SYM>
+__device__ __forceinline__ void had2(const double M[16], double E[16]) {
+  double T[16];  // T[i][b] = (M phi_b)_i
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double y[4];
+    had_n(M[4 * i], M[4 * i + 1], M[4 * i + 2], M[4 * i + 3], y);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) T[4 * i + b] = y[b];
+  }
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    double y[4];
+    had_n(T[b], T[4 + b], T[8 + b], T[12 + b], y);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) E[4 * a + b] = y[a];  // dead (a > b) entries are removed for SYM
+  }
+}
+
+__device__ __forceinline__ void cp_async8(unsigned saddr, const double* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(g) : "memory");
+}
+
+template <int KIND, int TC>
+__device__ __forceinline__ void element_had(const ElemH& K, int n, int ci, int cj, const double* __restrict__ v,
+                                            const double* __restrict__ vo, const double* __restrict__ pi,
+                                            const double* __restrict__ P, const double* __restrict__ rhoh,
+                                            double* __restrict__ Ks, double* __restrict__ Rs, int t) {
+  const int s = n + 1;
+  const long long Nc = (long long)n * n;
+  const int cell = cj * n + ci;
+  // All per-cell inputs are requested up front (one memory latency instead of one per Gauss
+  // point): pi(q, c) is staged asynchronously in this thread's Ks slot 24 + 3q + c (slot 9q + j
+  // is only written after pi(q) has been read), P and rho_i h in its Rs slots 0 and 1.
+  {
+    const unsigned ks = (unsigned)__cvta_generic_to_shared(Ks + t);
+    const unsigned rs = (unsigned)__cvta_generic_to_shared(Rs + t);
+    if (KIND == SEAICE_JAC_SV) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cp_async8(ks + (24 + 3 * q + c) * TC * 8, pi + (c * 4 + q) * Nc + cell);
+    }
+    cp_async8(rs, P + cell);
+    cp_async8(rs + TC * 8, rhoh + cell);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  double X[4], Y[4], WX[4], WY[4];  // modal coefficients of v_x, v_y and of w = v_o - v
+  {
+    const int nd0 = cj * s + ci;
+    double ux[4], uy[4], wx[4], wy[4];
+    const int ids[4] = {nd0, nd0 + 1, nd0 + s + 1, nd0 + s};
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const double2 a1 = __ldg(reinterpret_cast<const double2*>(v) + ids[b]);
+      const double2 a2 = __ldg(reinterpret_cast<const double2*>(vo) + ids[b]);
+      ux[b] = a1.x; uy[b] = a1.y;
+      wx[b] = a2.x - a1.x; wy[b] = a2.y - a1.y;
+    }
+    had_t(ux[0], ux[1], ux[2], ux[3], X);
+    had_t(uy[0], uy[1], uy[2], uy[3], Y);
+    had_t(wx[0], wx[1], wx[2], wx[3], WX);
+    had_t(wy[0], wy[1], wy[2], wy[3], WY);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  const double Pc = Rs[t], rh = Rs[TC + t];
+  // tau^(v)(q) = (A0 + eta A1 + xi A2, B0 + eta B1 - xi B2, C0 + xi B1 + eta B2)
+  const double A0 = K.ka * (X[1] + Y[2]), A1 = K.ka * X[3], A2 = K.ka * Y[3];
+  const double B0 = K.kb * (X[1] - Y[2]), B1 = K.kb * X[3], B2 = K.kb * Y[3];
+  const double C0 = K.kb * (X[2] + Y[1]);
+  X[0] *= 0.25; Y[0] *= 0.25; WX[0] *= 0.25; WY[0] *= 0.25;
+  const double scP = K.sc * Pc, mP = K.mwdtdx * Pc, hpw = K.hwdtdx * Pc, wrh = -K.w * rh;
+  double Ra[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) Ra[p] = 0.0;
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) {
+    double p11 = 0.0, p12 = 0.0, p22 = 0.0;
+    if (KIND == SEAICE_JAC_SV) {
+      const double* ps = Ks + (24 + 3 * q) * TC + t;
+      p11 = ps[0]; p12 = ps[TC]; p22 = ps[2 * TC];
+    }
+    const double xq = cQ[q].xq, eq = cQ[q].eq, x4 = cQ[q].x4, e4 = cQ[q].e4, xe4 = cQ[q].xe4;
+    const double vx = fma(x4, X[1], fma(e4, X[2], fma(xe4, X[3], X[0])));
+    const double vy = fma(x4, Y[1], fma(e4, Y[2], fma(xe4, Y[3], Y[0])));
+    const double wx = fma(x4, WX[1], fma(e4, WX[2], fma(xe4, WX[3], WX[0])));
+    const double wy = fma(x4, WY[1], fma(e4, WY[2], fma(xe4, WY[3], WY[0])));
+    const double tx = fma(xq, A2, fma(eq, A1, A0));
+    const double ty = fma(-xq, B2, fma(eq, B1, B0));
+    const double tz = fma(eq, B2, fma(xq, B1, C0));
+    const double X2 = fma(2.0, fma(tx, tx, fma(ty, ty, tz * tz)), K.dmin2);  // Delta^2 >= Delta_min^2 > 0
+    const double rD = rsqrt(X2);                                              // 1/Delta
+    const double alt = K.al * tx;
+    const double b1 = fma(K.be, ty, alt), b3 = fma(-K.be, ty, alt), b2 = K.be * tz;
+    const double cs = scP * rD;  // sc P/Delta
+    double Q11 = cs * K.pp11, Q13 = cs * K.pp13, Q22 = cs * K.pp22, Q33 = Q11, Q12 = 0.0, Q23 = 0.0;
+    if (KIND == SEAICE_JAC_SV) {
+      const double a1 = fma(K.ka1, p11, K.ka3 * p22), a3 = fma(K.ka3, p11, K.ka1 * p22), a2 = K.ka2 * p12;
+      const double pq = 2.0 * fma(p11, p11, fma(p22, p22, 2.0 * p12 * p12));  // 2 |pi^|^2
+      const double isf = pq > 1.0 ? rsqrt(pq) : 1.0;                            // 1/max(1, sqrt2 |pi^|)
+      const double mc1 = -(cs * rD * isf);                                       // -sc P/(Delta^2 s)
+      Q11 = fma(2.0 * mc1, a1 * b1, Q11);
+      Q22 = fma(2.0 * mc1, a2 * b2, Q22);
+      Q33 = fma(2.0 * mc1, a3 * b3, Q33);
+      Q12 = mc1 * fma(a1, b2, a2 * b1);
+      Q13 = fma(mc1, fma(a1, b3, a3 * b1), Q13);
+      Q23 = mc1 * fma(a2, b3, a3 * b2);
+    } else if (KIND == SEAICE_JAC_STD) {
+      const double mc1 = -2.0 * cs * (rD * rD);  // -sc 2P/Delta^3
+      Q11 = fma(mc1, b1 * b1, Q11);
+      Q22 = fma(mc1, b2 * b2, Q22);
+      Q33 = fma(mc1, b3 * b3, Q33);
+      Q12 = mc1 * (b1 * b2);
+      Q13 = fma(mc1, b1 * b3, Q13);
+      Q23 = mc1 * (b2 * b3);
+    }
+    double* slot = Ks + (9 * q) * TC + t;
+    slot[0 * TC] = Q11; slot[1 * TC] = Q12; slot[2 * TC] = Q13;
+    slot[3 * TC] = Q22; slot[4 * TC] = Q23; slot[5 * TC] = Q33;
+    // ocean drag linearisation C_o rho_o (|w| I + w w^T/|w|), w = v_o - v (eq:A), times w dt/16
+    const double n2 = fma(wx, wx, wy * wy);
+    double nw, r = 0.0;
+    if (n2 >= 1e-24) {  // |w| >= 1e-12
+      r = rsqrt(n2);
+      nw = n2 * r;
+    } else {
+      nw = sqrt(n2);
+    }
+    const double wxr = wx * r, wyr = wy * r;
+    slot[6 * TC] = K.kd * fma(wxr, wx, nw);
+    slot[7 * TC] = K.kd * fma(wyr, wy, nw);
+    slot[8 * TC] = K.kd * (wxr * wy);
+    // element residual -A(v, phi_{a,k}) (eq:A) = sum_a N_a MX + dN_a/dx CX + dN_a/dy CZ (x row)
+    const double wdcn = K.wdtco * nw;
+    const double MX = fma(wdcn, wx, wrh * vx), MY = fma(wdcn, wy, wrh * vy);
+    const double m = mP * rD;  // -w dt P/(Delta dx)
+    const double CX = fma(m, b1, hpw), CY = fma(m, b3, hpw), CZ = m * b2;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const double Na = cQ[q].N[a], gx = cQ[q].Gx[a], gy = cQ[q].Gy[a];
+      Ra[2 * a] = fma(Na, MX, fma(gx, CX, fma(gy, CZ, Ra[2 * a])));
+      Ra[2 * a + 1] = fma(Na, MY, fma(gy, CY, fma(gx, CZ, Ra[2 * a + 1])));
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < 8; ++p) Rs[p * TC + t] = Ra[p];
+  // q-moments of the parked values: mom[0] = sum, [1] = sum xi_q/g, [2] = sum eta_q/g, [3] = sum xi_q eta_q * 3
+  auto moments = [&](int j, double mom[4]) {
+    const double* sl = Ks + j * TC + t;
+    had_t(sl[0], sl[9 * TC], sl[18 * TC], sl[27 * TC], mom);
+  };
+  constexpr double g = kG, g2 = 1.0 / 3.0;
+  double S[15];  // s00 s01 s02 s11 s12 s22 s04 s05 s14 s15 s24 s25 s44 s45 s55
+  {
+    double q11[4], q12[4], q13[4], q22[4], q23[4], q33[4];
+    moments(0, q11); moments(1, q12); moments(2, q13); moments(3, q22); moments(4, q23); moments(5, q33);
+    S[0] = q11[0];
+    S[1] = q12[0];
+    S[2] = g * (q11[2] + q12[1]);
+    S[3] = q22[0];
+    S[4] = g * (q12[2] + q22[1]);
+    S[5] = g2 * ((q11[0] + q22[0]) + 2.0 * q12[3]);
+    S[6] = q13[0];
+    S[7] = g * (q12[2] + q13[1]);
+    S[8] = q23[0];
+    S[9] = g * (q22[2] + q23[1]);
+    S[10] = g * (q13[2] + q23[1]);
+    S[11] = g2 * ((q12[0] + q23[0]) + (q13[3] + q22[3]));
+    S[12] = q33[0];
+    S[13] = g * (q23[2] + q33[1]);
+    S[14] = g2 * ((q22[0] + q33[0]) + 2.0 * q23[3]);
+  }
+  // drag (+ mass) moment matrices (1/16 folded into kd, mass16): mu = (sum, sum xi, sum eta, sum xi eta)
+  auto md = [&](const double mu[4], double M[16]) {
+    const double m0 = mu[0], mx = g * mu[1], my = g * mu[2], mxy = g2 * mu[3];
+    M[0] = m0;       M[1] = mx;        M[2] = my;        M[3] = mxy;
+    M[4] = mx;       M[5] = g2 * m0;   M[6] = mxy;       M[7] = g2 * my;
+    M[8] = my;       M[9] = mxy;       M[10] = g2 * m0;  M[11] = g2 * mx;
+    M[12] = mxy;     M[13] = g2 * my;  M[14] = g2 * mx;  M[15] = (g2 * g2) * m0;
+  };
+  // S^xx = [s00 s01 s02; s01 s11 s12; s02 s12 s22], S^yy = [s11 s14 s15; s14 s44 s45; s15 s45 s55],
+  // S^xy = [s01 s04 s05; s11 s14 s15; s12 s24 s25]   (rows: x modes of a, cols: y modes of b)
+  const int sxx[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
+  const int syy[9] = {3, 8, 9, 8, 12, 13, 9, 13, 14};
+  const int sxy[9] = {1, 6, 7, 3, 8, 9, 4, 10, 11};
+  const double mass = K.mass16 * rh;
+  double mus[3][4];  // all parked values are read before the element matrix overwrites them
+  moments(6, mus[0]);  // d00
+  moments(7, mus[1]);  // d11
+  moments(8, mus[2]);  // d01
+  mus[0][0] += mass;
+  mus[1][0] += mass;
+#pragma unroll
+  for (int blk = 0; blk < 3; ++blk) {  // 0: xx, 1: yy, 2: xy
+    double M[16], E[16];
+    md(mus[blk], M);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int si = blk == 0 ? sxx[3 * r + c] : blk == 1 ? syy[3 * r + c] : sxy[3 * r + c];
+        M[4 * (r + 1) + (c + 1)] += S[si];
+      }
+    if (blk < 2) had2<true>(M, E);
+    else had2<false>(M, E);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if (blk == 0 && a <= b) Ks[ke_idx(2 * a, 2 * b) * TC + t] = E[4 * a + b];
+        if (blk == 1 && a <= b) Ks[ke_idx(2 * a + 1, 2 * b + 1) * TC + t] = E[4 * a + b];
+        if (blk == 2) {
+          if (a <= b) Ks[ke_idx(2 * a, 2 * b + 1) * TC + t] = E[4 * a + b];  // K_(a,x),(b,y)
+          else Ks[ke_idx(2 * b + 1, 2 * a) * TC + t] = E[4 * a + b];        // K_(b,y),(a,x)
+        }
+      }
+  }
+}
+
+// Phase 2 of the tiled kernels: the two rows of node (i, j) gathered from its four cells.
+template <int TX, int TC>
+__device__ __forceinline__ double gather_node_rows(int n, int Nn, int i0, int j0, int i, int j,
+                                                   const double* __restrict__ Ks, const double* __restrict__ Rs,
+                                                   const double* __restrict__ F, double* __restrict__ Jst,
+                                                   double* __restrict__ R) {
+  const int s = n + 1;
+  const int node = j * s + i;
+  if (!(i > 0 && i < n && j > 0 && j < n)) {
+#pragma unroll
+    for (int e = 0; e < 36; ++e) Jst[(long long)e * Nn + node] = (e == 16 || e == 19) ? 1.0 : 0.0;
+    R[2 * node] = 0.0;
+    R[2 * node + 1] = 0.0;
+    return 0.0;
+  }
+  // cell cc at offset (cc&1, cc>>1) from (i-1, j-1); the node is its local corner (1-ox, 1-oy)
+  const int lc0 = (i - i0) + (j - j0) * (TX + 1);
+  double r0 = F[2 * node], r1 = F[2 * node + 1];
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc) {
+    const int a = lidx(1 - (cc & 1), 1 - (cc >> 1));
+    const int lc = lc0 + (cc & 1) + (cc >> 1) * (TX + 1);
+    r0 += Rs[(2 * a) * TC + lc];
+    r1 += Rs[(2 * a + 1) * TC + lc];
+  }
+  R[2 * node] = r0;
+  R[2 * node + 1] = r1;
+#pragma unroll
+  for (int sl = 0; sl < 9; ++sl) {
+    const int dxs = sl % 3 - 1, dys = sl / 3 - 1;
+    const bool bnd = (i + dxs == 0 || i + dxs == n || j + dys == 0 || j + dys == n);  // symmetric elimination
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k = e >> 1, m = e & 1;
+      double acc = 0.0;
+      bool first = true;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int ax = 1 - (cc & 1), ay = 1 - (cc >> 1);
+        const int bx = ax + dxs, by = ay + dys;
+        if (bx < 0 || bx > 1 || by < 0 || by > 1) continue;
+        const int p = 2 * lidx(ax, ay) + k, q = 2 * lidx(bx, by) + m;
+        const int lc = lc0 + (cc & 1) + (cc >> 1) * (TX + 1);
+        const double val = Ks[(p <= q ? ke_idx(p, q) : ke_idx(q, p)) * TC + lc];
+        acc = first ? val : acc + val;  // no 0.0 + x (not foldable under IEEE signed zeros)
+        first = false;
+      }
+      Jst[(long long)(sl * 4 + e) * Nn + node] = bnd ? 0.0 : acc;
+    }
+  }
+  return r0 * r0 + r1 * r1;
+}
+
+// Persistent form: 2 CTAs per SM loop over the tiles (fixed assignment => fixed summation order
+// of the residual norm); while a tile is assembled, the next tile's inputs are prefetched into L2.
+template <int TX, int TY>
+struct HadTile {
+  static constexpr int TC = (TX + 1) * (TY + 1), NT = TC, SMEM = (kKE + 8) * TC * 8;
+};
+
+template <int KIND, int TX, int TY>
+__global__ void __launch_bounds__(HadTile<TX, TY>::NT, 2)
+    k_assemble_had(Phys ph, ElemH K, int Nn, int tiles_x, int ntiles, const double* __restrict__ v,
+                   const double* __restrict__ pi, const double* __restrict__ P, const double* __restrict__ rhoh,
+                   const double* __restrict__ vo, const double* __restrict__ F, double* __restrict__ Jst,
+                   double* __restrict__ R, double* __restrict__ part) {
+  constexpr int TC = HadTile<TX, TY>::TC;
+  extern __shared__ double smem[];
+  double* Ks = smem;             // [36][TC]
+  double* Rs = smem + kKE * TC;  // [8][TC]
+  __shared__ double sh[32];
+  const int n = ph.n, s = n + 1;
+  const long long Nc = (long long)n * n;
+  const int t = threadIdx.x;
+  double nrm = 0.0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int i0 = (tile % tiles_x) * TX, j0 = (tile / tiles_x) * TY;
+    {
+      const int ci = i0 - 1 + t % (TX + 1), cj = j0 - 1 + t / (TX + 1);
+      if (ci >= 0 && ci < n && cj >= 0 && cj < n) element_had<KIND, TC>(K, n, ci, cj, v, vo, pi, P, rhoh, Ks, Rs, t);
+    }
+    {
+      const int nt = tile + gridDim.x;
+      if (nt < ntiles) {
+        const int ci = (nt % tiles_x) * TX - 1 + t % (TX + 1), cj = (nt / tiles_x) * TY - 1 + t / (TX + 1);
+        if (ci >= 0 && ci < n && cj >= 0 && cj < n) {
+          const int cell = cj * n + ci, nd = cj * s + ci;
+          if (KIND == SEAICE_JAC_SV) {
+#pragma unroll
+            for (int r = 0; r < 12; ++r) asm volatile("prefetch.global.L2 [%0];" ::"l"(pi + r * Nc + cell));
+          }
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(P + cell));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(rhoh + cell));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(v + 2 * nd));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(v + 2 * (nd + s)));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(vo + 2 * nd));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(vo + 2 * (nd + s)));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(F + 2 * (nd + s + 1)));
+        }
+      }
+    }
+    __syncthreads();
+    if (t < TX * TY) {
+      const int i = i0 + t % TX, j = j0 + t / TX;
+      if (i <= n && j <= n) nrm += gather_node_rows<TX, TC>(n, Nn, i0, j0, i, j, Ks, Rs, F, Jst, R);
+    }
+    __syncthreads();  // Ks / Rs are rewritten by the next tile
+  }
+  const double bs = block_sum(nrm, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = bs;
+}
+
+template <int KIND, int TX, int TY>
+static int launch_assemble_had_t(Ctx& c, const double* v, const double* pi, double* R) {
+  using HT = HadTile<TX, TY>;
+  static int ctas = 0;
+  if (!ctas) {
+    SI_CUDA(cudaFuncSetAttribute(k_assemble_had<KIND, TX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, HT::SMEM));
+    int per_sm = 0, dev = 0, sms = 0;
+    SI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_assemble_had<KIND, TX, TY>, HT::NT, HT::SMEM));
+    SI_CUDA(cudaGetDevice(&dev));
+    SI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    ctas = (per_sm > 0 ? per_sm : 1) * sms;
+  }
+  upload_qc();
+  const int tx = (c.n + 1 + TX - 1) / TX, ty = (c.n + 1 + TY - 1) / TY;
+  const int ntiles = tx * ty;
+  static const bool persist = getenv("SEAICE_ASM_PERSIST") && atoi(getenv("SEAICE_ASM_PERSIST"));  // tuning aid
+  const int g = (persist && ctas < ntiles) ? ctas : ntiles;
+  c.part.ensure(c.al, g + 64);
+  prof_begin(c);
+  k_assemble_had<KIND, TX, TY><<<g, HT::NT, HT::SMEM, c.s>>>(c.ph, make_elemh(c.ph), c.Nn, tx, ntiles, v, pi, c.P.get(),
+                                                             c.rhoh.get(), c.vocean.get(), c.F.get(), c.Jst.get(), R,
+                                                             c.part.get());
+  SI_LAUNCHED(c);
+  prof_end(c, PC_ASSEMBLE, 352.0 * c.Nn + 112.0 * c.Nc);
+  return g;
+}
+
+template <int KIND>
+static int launch_assemble_had(Ctx& c, const double* v, const double* pi, double* R) {
+  static const int variant = getenv("SEAICE_ASM_TILE") ? atoi(getenv("SEAICE_ASM_TILE")) : 0;  // tuning aid
+  if (variant == 1) return launch_assemble_had_t<KIND, 15, 16>(c, v, pi, R);
+  return launch_assemble_had_t<KIND, 31, 8>(c, v, pi, R);
+}
+
 template <int KIND>
 static int launch_assemble_modal(Ctx& c, const double* v, const double* pi, double* R) {
   static bool attr = false;
@@ -1041,12 +1502,16 @@ void assemble_impl(Ctx& c, const double* v, const double* pi, bool jac, double* 
     if (kind == SEAICE_JAC_SV) nparts = launch_assemble_tiled<SEAICE_JAC_SV>(c, v, pp, R);
     else if (kind == SEAICE_JAC_STD) nparts = launch_assemble_tiled<SEAICE_JAC_STD>(c, v, pp, R);
     else nparts = launch_assemble_tiled<SEAICE_JAC_PICARD>(c, v, pp, R);
+  } else if (getenv("SEAICE_ASM_MODAL")) {
+    if (kind == SEAICE_JAC_SV) nparts = launch_assemble_modal<SEAICE_JAC_SV>(c, v, pp, R);
+    else if (kind == SEAICE_JAC_STD) nparts = launch_assemble_modal<SEAICE_JAC_STD>(c, v, pp, R);
+    else nparts = launch_assemble_modal<SEAICE_JAC_PICARD>(c, v, pp, R);
   } else if (kind == SEAICE_JAC_SV) {
-    nparts = launch_assemble_modal<SEAICE_JAC_SV>(c, v, pp, R);
+    nparts = launch_assemble_had<SEAICE_JAC_SV>(c, v, pp, R);
   } else if (kind == SEAICE_JAC_STD) {
-    nparts = launch_assemble_modal<SEAICE_JAC_STD>(c, v, pp, R);
+    nparts = launch_assemble_had<SEAICE_JAC_STD>(c, v, pp, R);
   } else {
-    nparts = launch_assemble_modal<SEAICE_JAC_PICARD>(c, v, pp, R);
+    nparts = launch_assemble_had<SEAICE_JAC_PICARD>(c, v, pp, R);
   }
   if (r_out) {
     SI_CUDA(cudaMemcpyAsync(r_out, R, sizeof(double) * c.N, cudaMemcpyDeviceToDevice, c.s));

@@ -182,7 +182,7 @@ def run_reference(a, rank, world):
 
 # ----------------------------------------------------------------------------- our arm
 BYTES_NOTE = {
-    "cheb0": "finest-level fused Chebyshev step: 9 stencil slots x 2x2 fp64 (288 B/node) + vector traffic per variant",
+    "cheb0": "finest-level Chebyshev steps: symmetric stencil, 19 fp64 per node (152 B/node, stencil.cuh) + vector traffic per variant",
 }
 
 

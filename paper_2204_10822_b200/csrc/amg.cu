@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "ctx.cuh"
+#include "stencil.cuh"
 
 namespace seaice {
 
@@ -88,14 +89,14 @@ __global__ void k_stencil_to_bsr(int n, int Nn, const double* __restrict__ Jst, 
   const bool interior = (i > 0 && i < n && j > 0 && j < n);
   long long o = (long long)rp[node] * 4;
   if (!interior) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) val[o + e] = Jst[(16LL + e) * Nn + node];
+    const double4 D = stencil_diag(Jst, Nn, node);
+    val[o] = D.x; val[o + 1] = D.y; val[o + 2] = D.z; val[o + 3] = D.w;
     return;
   }
+  double Jr[36];
+  stencil_row(Jst, Nn, s, node, Jr);
 #pragma unroll
-  for (int sl = 0; sl < 9; ++sl)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) val[o + sl * 4 + e] = Jst[(long long)(sl * 4 + e) * Nn + node];
+  for (int e = 0; e < 36; ++e) val[o + e] = Jr[e];
 }
 
 static void build_level0_pattern(Ctx& c, Level& L) {
@@ -1120,20 +1121,15 @@ __global__ void __launch_bounds__(256) k_cheb_stencil(int n, int Nn, const doubl
   x[node] = xv;
   if (!want_r) return;
   const int s = n + 1, i = node % s, j = node / s;
-  double y0 = 0.0, y1 = 0.0;
+  double y0, y1;
   if (i > 0 && i < n && j > 0 && j < n) {
-#pragma unroll
-    for (int sl = 0; sl < 9; ++sl) {
-      const int nb = node + (sl / 3 - 1) * s + (sl % 3 - 1);
-      const double2 v = __ldg(d + nb);
-      const double* Js = J + (long long)sl * 4 * Nn + node;
-      y0 += __ldg(Js) * v.x + __ldg(Js + Nn) * v.y;
-      y1 += __ldg(Js + 2LL * Nn) * v.x + __ldg(Js + 3LL * Nn) * v.y;
-    }
+    const double2 y = stencil_apply(J, Nn, s, node, d);
+    y0 = y.x;
+    y1 = y.y;
   } else {
-    const double* Js = J + 16LL * Nn + node;
-    y0 = Js[0] * dv.x + Js[Nn] * dv.y;
-    y1 = Js[2LL * Nn] * dv.x + Js[3LL * Nn] * dv.y;
+    const double4 D = stencil_diag(J, Nn, node);
+    y0 = D.x * dv.x + D.y * dv.y;
+    y1 = D.z * dv.x + D.w * dv.y;
   }
   double2 rv = r[node];
   rv.x -= y0;
@@ -1216,11 +1212,12 @@ __global__ void __launch_bounds__(FusedGeom<M>::NT, (FusedGeom<M>::NT <= 256 ? 2
   double4 D = make_double4(0.0, 0.0, 0.0, 0.0);
   if (inside) {
     if (interior) {
-#pragma unroll
-      for (int e = 0; e < 36; ++e) Jr[e] = __ldg(J + (long long)e * Nn + node);
+      stencil_row(J, Nn, s, node, Jr);
     } else {
+      const double4 Dg = stencil_diag(J, Nn, node);
 #pragma unroll
-      for (int e = 0; e < 36; ++e) Jr[e] = (e >= 16 && e < 20) ? __ldg(J + (long long)e * Nn + node) : 0.0;
+      for (int e = 0; e < 36; ++e) Jr[e] = 0.0;
+      Jr[16] = Dg.x; Jr[17] = Dg.y; Jr[18] = Dg.z; Jr[19] = Dg.w;
     }
     rv = rin[node];
     D = reinterpret_cast<const double4*>(dinv)[node];
@@ -1307,21 +1304,16 @@ __global__ void __launch_bounds__(256) k_resid_dinv_stencil(int n, int Nn, const
   double2 rv = b[node];
   if (x) {
     const int s = n + 1, i = node % s, j = node / s;
-    double y0 = 0.0, y1 = 0.0;
+    double y0, y1;
     if (i > 0 && i < n && j > 0 && j < n) {
-#pragma unroll
-      for (int sl = 0; sl < 9; ++sl) {
-        const int nb = node + (sl / 3 - 1) * s + (sl % 3 - 1);
-        const double2 v = __ldg(x + nb);
-        const double* Js = J + (long long)sl * 4 * Nn + node;
-        y0 += __ldg(Js) * v.x + __ldg(Js + Nn) * v.y;
-        y1 += __ldg(Js + 2LL * Nn) * v.x + __ldg(Js + 3LL * Nn) * v.y;
-      }
+      const double2 y = stencil_apply(J, Nn, s, node, x);
+      y0 = y.x;
+      y1 = y.y;
     } else {
       const double2 v = x[node];
-      const double* Js = J + 16LL * Nn + node;
-      y0 = Js[0] * v.x + Js[Nn] * v.y;
-      y1 = Js[2LL * Nn] * v.x + Js[3LL * Nn] * v.y;
+      const double4 D = stencil_diag(J, Nn, node);
+      y0 = D.x * v.x + D.y * v.y;
+      y1 = D.z * v.x + D.w * v.y;
     }
     rv.x -= y0;
     rv.y -= y1;
@@ -1904,7 +1896,7 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
     SI_LAUNCHED(c);
     const double B = L.b;
     double by = L.nb * (8.0 * B * 3 + 8.0 * B * B);  // b read, r write, d write, dinv
-    if (!pre) by += L.nnzb * (8.0 * B * B + (st ? 0.0 : 4.0)) + (st ? 0.0 : 4.0 * (L.nb + 1)) + 8.0 * B * L.nb;
+    if (!pre) by += (st ? kJBytesNode * c.Nn : L.nnzb * (8.0 * B * B + 4.0) + 4.0 * (L.nb + 1)) + 8.0 * B * L.nb;
     prof_end(c, st ? PC_RESID0 : PC_RESIDC, by);
   }
   if (fused) {
@@ -1927,7 +1919,7 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
     }
     SI_LAUNCHED(c);
     // algorithmic bytes: stencil + Dinv once, r_0 / b read (+ d_0, x_0 for post), x (+ r_m) written
-    prof_end(c, PC_CHEB0F, (double)c.Nn * (288.0 + 32.0 + 16.0 + (pre ? 32.0 : 48.0)));
+    prof_end(c, PC_CHEB0F, (double)c.Nn * (kJBytesNode + 32.0 + 16.0 + (pre ? 32.0 : 48.0)));
     return;
   }
   for (int it = 0; it < m; ++it) {
@@ -1952,7 +1944,7 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
     {
       const double B = L.b;
       double by = L.nb * 8.0 * B * (first ? 2.0 : 3.0);  // d read, x (read +) write
-      if (want_r) by += L.nnzb * (8.0 * B * B + (st ? 0.0 : 4.0)) + (st ? 0.0 : 4.0 * (L.nb + 1)) + 16.0 * B * L.nb;
+      if (want_r) by += (st ? kJBytesNode * c.Nn : L.nnzb * (8.0 * B * B + 4.0) + 4.0 * (L.nb + 1)) + 16.0 * B * L.nb;
       if (want_d) by += L.nb * (8.0 * B * B + 8.0 * B);
       prof_end(c, st ? PC_CHEB0 : PC_CHEBC, by);
     }

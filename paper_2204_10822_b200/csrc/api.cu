@@ -5,6 +5,7 @@
 #include <vector>
 
 #include "ctx.cuh"
+#include "stencil.cuh"
 
 using namespace seaice;
 
@@ -261,7 +262,7 @@ int seaice_create(const seaice_params* p, const seaice_runtime* rt, seaice_ctx**
     c.vocean.ensure(c.al, c.N);
     c.pi.ensure(c.al, 12LL * c.Nc);
     c.flag.ensure(c.al, 16);
-    c.Jst.ensure(c.al, 36LL * c.Nn);
+    c.Jst.ensure(c.al, (long long)kJS * c.Nn);
     c.R.ensure(c.al, c.N);
     c.scal.ensure(c.al, 256);
     c.part.ensure(c.al, 4096);

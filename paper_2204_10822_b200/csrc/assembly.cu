@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "ctx.cuh"
+#include "stencil.cuh"
 
 namespace seaice {
 
@@ -138,19 +139,15 @@ __global__ void k_pi_init(Phys ph, int Nc, const double* __restrict__ v, double*
 #undef PI_Q
 }
 
-// ------------------------------------------------------------------ K1
-// Contribution of one cell to the two residual rows and 2x8 Jacobian row block of
-// its local node AL (eq:A + eq:sigma for R; eq:linearSVNewton/-modification for K):
+// ------------------------------------------------------------------ K1 (residual only)
+// Contribution of one cell to the two residual rows of its local node AL (eq:A + eq:sigma):
 //   R_k  -= sum_q w [rho h v_k N_a + dt (P/Delta) tau^(v).tau^(N_a e_k) - dt (P/2) dN_a/dx_k
 //                    - dt C_o rho_o |w| w_k N_a]
-//   K_km += sum_q w [rho h N_a N_b d_km + dt tau^(N_a e_k).C tau^(N_b e_m) + dt N_a N_b D_km]
-template <int KIND, bool JAC, int AL>
-__device__ __forceinline__ void assemble_cell(const Phys& ph, int ci, int cj, const double* __restrict__ v,
-                                              const double* __restrict__ pi, const double* __restrict__ P,
-                                              const double* __restrict__ rhoh, const double* __restrict__ vo,
-                                              double acc[36], double& r0, double& r1) {
+template <int AL>
+__device__ __forceinline__ void residual_cell(const Phys& ph, int ci, int cj, const double* __restrict__ v,
+                                              const double* __restrict__ P, const double* __restrict__ rhoh,
+                                              const double* __restrict__ vo, double& r0, double& r1) {
   const int n = ph.n;
-  const long long Nc = (long long)n * n;
   const int cell = cj * n + ci;
   double u[4][2], uo[4][2];
   load_cell_vec(v, n, ci, cj, u);
@@ -183,67 +180,20 @@ __device__ __forceinline__ void assemble_cell(const Phys& ph, int ci, int cj, co
     const V3 t = tau_hat_grad(L00, L01, L10, L11, inv_e);
     const double D = sqrt(dmin2 + 2.0 * dot3(t, t));
     const double c0 = Pc / D;
-    // ocean drag
     const double wx = ox_ - vx, wy = oy_ - vy;
     const double nw = sqrt(wx * wx + wy * wy);
-    // test-function tau^ of node AL
     const double gxa = Gx(q, AL) * inv_dx, gya = Gy(q, AL) * inv_dx;
     const V3 ta0 = tau_hat_ex(gxa, gya, inv_e);
     const V3 ta1 = tau_hat_ey(gxa, gya, inv_e);
     const double Na = Nq(q, AL);
-    // residual: R -= A(v, phi)
     r0 -= w * (rh * vx * Na + dt * c0 * dot3(t, ta0) - dt * 0.5 * Pc * gxa - dt * co * nw * wx * Na);
     r1 -= w * (rh * vy * Na + dt * c0 * dot3(t, ta1) - dt * 0.5 * Pc * gya - dt * co * nw * wy * Na);
-    if (JAC) {
-      // u_k = C tau^(N_a e_k)
-      V3 u0 = ta0, u1 = ta1;
-      u0.x *= c0; u0.y *= c0; u0.z *= c0;
-      u1.x *= c0; u1.y *= c0; u1.z *= c0;
-      if (KIND == SEAICE_JAC_SV) {
-        const V3 p = pi_hat(pi[(0 * 4 + q) * Nc + cell], pi[(1 * 4 + q) * Nc + cell], pi[(2 * 4 + q) * Nc + cell]);
-        const double s = fmax(1.0, kR2 * sqrt(dot3(p, p)));
-        const double c1 = Pc / (D * D * s);
-        const double tt0 = dot3(t, ta0), pt0 = dot3(p, ta0);
-        const double tt1 = dot3(t, ta1), pt1 = dot3(p, ta1);
-        u0.x -= c1 * (p.x * tt0 + t.x * pt0); u0.y -= c1 * (p.y * tt0 + t.y * pt0); u0.z -= c1 * (p.z * tt0 + t.z * pt0);
-        u1.x -= c1 * (p.x * tt1 + t.x * pt1); u1.y -= c1 * (p.y * tt1 + t.y * pt1); u1.z -= c1 * (p.z * tt1 + t.z * pt1);
-      } else if (KIND == SEAICE_JAC_STD) {
-        const double c1 = 2.0 * Pc / (D * D * D);
-        const double tt0 = dot3(t, ta0), tt1 = dot3(t, ta1);
-        u0.x -= c1 * t.x * tt0; u0.y -= c1 * t.y * tt0; u0.z -= c1 * t.z * tt0;
-        u1.x -= c1 * t.x * tt1; u1.y -= c1 * t.y * tt1; u1.z -= c1 * t.z * tt1;
-      }
-      // drag coefficient D_km = C_o rho_o (|w| d_km + w_k w_m / |w|), rank-one part dropped if |w| < 1e-12
-      double d00 = co * nw, d11 = co * nw, d01 = 0.0;
-      if (nw >= 1e-12) {
-        const double inw = co / nw;
-        d00 += inw * wx * wx;
-        d11 += inw * wy * wy;
-        d01 = inw * wx * wy;
-      }
-      const double wdt = w * dt;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int sl = slot_ab(AL, b);
-        const double gxb = Gx(q, b) * inv_dx, gyb = Gy(q, b) * inv_dx;
-        const V3 tb0 = tau_hat_ex(gxb, gyb, inv_e);
-        const V3 tb1 = tau_hat_ey(gxb, gyb, inv_e);
-        const double NN = Na * Nq(q, b);
-        const double mass = w * rh * NN;
-        acc[sl * 4 + 0] += mass + wdt * (dot3(u0, tb0) + NN * d00);
-        acc[sl * 4 + 1] += wdt * (dot3(u0, tb1) + NN * d01);
-        acc[sl * 4 + 2] += wdt * (dot3(u1, tb0) + NN * d01);
-        acc[sl * 4 + 3] += mass + wdt * (dot3(u1, tb1) + NN * d11);
-      }
-    }
   }
 }
 
-template <int KIND, bool JAC>
-__global__ void __launch_bounds__(128) k_assemble(Phys ph, int Nn, const double* __restrict__ v,
-                                                  const double* __restrict__ pi, const double* __restrict__ P,
-                                                  const double* __restrict__ rhoh, const double* __restrict__ vo,
-                                                  const double* __restrict__ F, double* __restrict__ Jst,
+__global__ void __launch_bounds__(128) k_residual(Phys ph, int Nn, const double* __restrict__ v,
+                                                  const double* __restrict__ P, const double* __restrict__ rhoh,
+                                                  const double* __restrict__ vo, const double* __restrict__ F,
                                                   double* __restrict__ R, double* __restrict__ part) {
   __shared__ double sh[32];
   const int node = blockIdx.x * blockDim.x + threadIdx.x;
@@ -253,33 +203,17 @@ __global__ void __launch_bounds__(128) k_assemble(Phys ph, int Nn, const double*
     const int i = node % s, j = node / s;
     const bool interior = (i > 0 && i < ph.n && j > 0 && j < ph.n);
     if (!interior) {
-      if (JAC) {
-#pragma unroll
-        for (int e = 0; e < 36; ++e) Jst[(long long)e * Nn + node] = (e == 16 || e == 19) ? 1.0 : 0.0;
-      }
       R[2 * node] = 0.0;
       R[2 * node + 1] = 0.0;
     } else {
-      double acc[36];
-#pragma unroll
-      for (int e = 0; e < 36; ++e) acc[e] = 0.0;
       double r0 = F[2 * node], r1 = F[2 * node + 1];
-      assemble_cell<KIND, JAC, 2>(ph, i - 1, j - 1, v, pi, P, rhoh, vo, acc, r0, r1);
-      assemble_cell<KIND, JAC, 3>(ph, i, j - 1, v, pi, P, rhoh, vo, acc, r0, r1);
-      assemble_cell<KIND, JAC, 1>(ph, i - 1, j, v, pi, P, rhoh, vo, acc, r0, r1);
-      assemble_cell<KIND, JAC, 0>(ph, i, j, v, pi, P, rhoh, vo, acc, r0, r1);
+      residual_cell<2>(ph, i - 1, j - 1, v, P, rhoh, vo, r0, r1);
+      residual_cell<3>(ph, i, j - 1, v, P, rhoh, vo, r0, r1);
+      residual_cell<1>(ph, i - 1, j, v, P, rhoh, vo, r0, r1);
+      residual_cell<0>(ph, i, j, v, P, rhoh, vo, r0, r1);
       R[2 * node] = r0;
       R[2 * node + 1] = r1;
       nrm = r0 * r0 + r1 * r1;
-      if (JAC) {
-#pragma unroll
-        for (int sl = 0; sl < 9; ++sl) {
-          const int ii = i + (sl % 3) - 1, jj = j + (sl / 3) - 1;
-          const bool bnd = (ii == 0 || ii == ph.n || jj == 0 || jj == ph.n);  // symmetric elimination
-#pragma unroll
-          for (int e = 0; e < 4; ++e) Jst[(long long)(sl * 4 + e) * Nn + node] = bnd ? 0.0 : acc[sl * 4 + e];
-        }
-      }
     }
   }
   double bs = block_sum(nrm, sh);
@@ -443,8 +377,10 @@ __global__ void k_csr_values(int n, int Nn, const double* __restrict__ Jst, cons
       val[o] = 1.0;
       continue;
     }
+    double Jr[36];
+    stencil_row(Jst, Nn, s, node, Jr);
     for (int sl = 0; sl < 9; ++sl)
-      for (int m = 0; m < 2; ++m) val[o++] = Jst[(long long)(sl * 4 + k * 2 + m) * Nn + node];
+      for (int m = 0; m < 2; ++m) val[o++] = Jr[sl * 4 + k * 2 + m];
   }
 }
 
@@ -495,503 +431,39 @@ void set_step_impl(Ctx& c, double dt, double t_new, const double* h, const doubl
   c.have_r0 = false;
 }
 
-// ------------------------------------------------------------------ K1, tiled (Jacobian path)
-// Two-phase, atomics-free: a CTA owns a 31 x 8 tile of nodes.  Phase 1: one thread per cell of
-// the 32 x 9 cells touching the tile computes the packed 8x8 element matrix (upper triangle,
-// 36 values) and the 8 element residual terms into shared memory (SoA, bank-conflict free).
-// Phase 2: one thread per node gathers its two rows from the four adjacent cells, writes the
-// 36 stencil slots (coalesced) and its two residual entries.  Each cell's quadrature-point
-// algebra is done once per tile (1.16x recompute for the halo) instead of once per node (4x).
-constexpr int kTX = 31, kTY = 8, kTC = (kTX + 1) * (kTY + 1);  // 248 nodes, 288 cells
-constexpr int kTThreads = kTC;
-constexpr int kKE = 36;
-__host__ __device__ constexpr int ke_idx(int p, int q) { return p * 8 - p * (p - 1) / 2 + (q - p); }  // p <= q
-constexpr size_t kTileSmem = (size_t)(kKE + 8) * kTC * sizeof(double);
-
-template <int KIND>
-__global__ void __launch_bounds__(kTThreads, 2) k_assemble_tiled(Phys ph, int Nn, const double* __restrict__ v,
-                                                                  const double* __restrict__ pi,
-                                                                  const double* __restrict__ P,
-                                                                  const double* __restrict__ rhoh,
-                                                                  const double* __restrict__ vo,
-                                                                  const double* __restrict__ F,
-                                                                  double* __restrict__ Jst, double* __restrict__ R,
-                                                                  double* __restrict__ part) {
-  extern __shared__ double smem[];
-  double* Ks = smem;             // [36][kTC]
-  double* Rs = smem + kKE * kTC;  // [8][kTC]
-  __shared__ double sh[32];
-  const int n = ph.n, s = n + 1;
-  const int i0 = blockIdx.x * kTX, j0 = blockIdx.y * kTY;
-  const int t = threadIdx.x;
-  // ---- phase 1: element matrix and element residual of cell t
-  {
-    const int ci = i0 - 1 + t % (kTX + 1), cj = j0 - 1 + t / (kTX + 1);
-    if (ci >= 0 && ci < n && cj >= 0 && cj < n) {
-      const long long Nc = (long long)n * n;
-      const int cell = cj * n + ci;
-      double u[4][2], uo[4][2];
-      {
-        const int nd0 = cj * s + ci;
-        const int ids[4] = {nd0, nd0 + 1, nd0 + s + 1, nd0 + s};
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const double2 a1 = __ldg(reinterpret_cast<const double2*>(v) + ids[b]);
-          const double2 a2 = __ldg(reinterpret_cast<const double2*>(vo) + ids[b]);
-          u[b][0] = a1.x; u[b][1] = a1.y; uo[b][0] = a2.x; uo[b][1] = a2.y;
-        }
-      }
-      const double Pc = P[cell], rh = rhoh[cell];
-      const double inv_dx = 1.0 / ph.dx, inv_e = 1.0 / ph.e;
-      const double w = 0.25 * ph.dx * ph.dx;
-      const double co = ph.C_o * ph.rho_o;
-      const double dt = ph.dt;
-      const double dmin2 = ph.delta_min * ph.delta_min;
-#pragma unroll 1
-      for (int q = 0; q < 4; ++q) {
-        double vx = 0, vy = 0, ox_ = 0, oy_ = 0, L00 = 0, L01 = 0, L10 = 0, L11 = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          vx += Nq(q, b) * u[b][0];
-          vy += Nq(q, b) * u[b][1];
-          ox_ += Nq(q, b) * uo[b][0];
-          oy_ += Nq(q, b) * uo[b][1];
-          L00 += u[b][0] * Gx(q, b);
-          L01 += u[b][0] * Gy(q, b);
-          L10 += u[b][1] * Gx(q, b);
-          L11 += u[b][1] * Gy(q, b);
-        }
-        L00 *= inv_dx; L01 *= inv_dx; L10 *= inv_dx; L11 *= inv_dx;
-        const V3 tq = tau_hat_grad(L00, L01, L10, L11, inv_e);
-        const double D = sqrt(dmin2 + 2.0 * dot3(tq, tq));
-        const double c0 = Pc / D;
-        const double wx = ox_ - vx, wy = oy_ - vy;
-        const double nw = sqrt(wx * wx + wy * wy);
-        double d00 = co * nw, d11 = co * nw, d01 = 0.0;
-        if (nw >= 1e-12) {
-          const double inw = co / nw;
-          d00 += inw * wx * wx;
-          d11 += inw * wy * wy;
-          d01 = inw * wx * wy;
-        }
-        // linearised stress coefficient C (symmetric 3x3)
-        double C00 = c0, C11 = c0, C22 = c0, C01 = 0.0, C02 = 0.0, C12 = 0.0;
-        if (KIND == SEAICE_JAC_SV) {
-          const V3 p = pi_hat(pi[(0 * 4 + q) * Nc + cell], pi[(1 * 4 + q) * Nc + cell], pi[(2 * 4 + q) * Nc + cell]);
-          const double sc = fmax(1.0, kR2 * sqrt(dot3(p, p)));
-          const double c1 = Pc / (D * D * sc);
-          C00 -= c1 * 2.0 * p.x * tq.x; C11 -= c1 * 2.0 * p.y * tq.y; C22 -= c1 * 2.0 * p.z * tq.z;
-          C01 -= c1 * (p.x * tq.y + tq.x * p.y);
-          C02 -= c1 * (p.x * tq.z + tq.x * p.z);
-          C12 -= c1 * (p.y * tq.z + tq.y * p.z);
-        } else if (KIND == SEAICE_JAC_STD) {
-          const double c1 = 2.0 * Pc / (D * D * D);
-          C00 -= c1 * tq.x * tq.x; C11 -= c1 * tq.y * tq.y; C22 -= c1 * tq.z * tq.z;
-          C01 -= c1 * tq.x * tq.y; C02 -= c1 * tq.x * tq.z; C12 -= c1 * tq.y * tq.z;
-        }
-        // test-function tau^ for the 8 local DOFs p = 2a + k
-        V3 tb[8];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const double gx = Gx(q, a) * inv_dx, gy = Gy(q, a) * inv_dx;
-          tb[2 * a] = tau_hat_ex(gx, gy, inv_e);
-          tb[2 * a + 1] = tau_hat_ey(gx, gy, inv_e);
-        }
-        const double wdt = w * dt;
-#pragma unroll
-        for (int qq = 0; qq < 8; ++qq) {
-          const V3& x = tb[qq];
-          const V3 uq{C00 * x.x + C01 * x.y + C02 * x.z, C01 * x.x + C11 * x.y + C12 * x.z,
-                      C02 * x.x + C12 * x.y + C22 * x.z};
-          const int b = qq >> 1, m = qq & 1;
-#pragma unroll
-          for (int pp = 0; pp <= qq; ++pp) {
-            const int a = pp >> 1, k = pp & 1;
-            const double NN = Nq(q, a) * Nq(q, b);
-            double val = wdt * dot3(tb[pp], uq);
-            if (k == m) val += w * rh * NN + wdt * NN * (k == 0 ? d00 : d11);
-            else val += wdt * NN * d01;
-            double* dst = Ks + ke_idx(pp, qq) * kTC + t;
-            *dst = (q == 0) ? val : *dst + val;
-          }
-        }
-        // element residual: -A(v, phi_p)
-#pragma unroll
-        for (int pp = 0; pp < 8; ++pp) {
-          const int a = pp >> 1, k = pp & 1;
-          const double Na = Nq(q, a);
-          const double g = (k == 0 ? Gx(q, a) : Gy(q, a)) * inv_dx;
-          const double val = -w * (rh * (k == 0 ? vx : vy) * Na + dt * c0 * dot3(tq, tb[pp]) - dt * 0.5 * Pc * g -
-                                   dt * co * nw * (k == 0 ? wx : wy) * Na);
-          double* dst = Rs + pp * kTC + t;
-          *dst = (q == 0) ? val : *dst + val;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  // ---- phase 2: rows of node t
-  double nrm = 0.0;
-  if (t < kTX * kTY) {
-    const int i = i0 + t % kTX, j = j0 + t / kTX;
-    if (i <= n && j <= n) {
-      const int node = j * s + i;
-      if (!(i > 0 && i < n && j > 0 && j < n)) {
-#pragma unroll
-        for (int e = 0; e < 36; ++e) Jst[(long long)e * Nn + node] = (e == 16 || e == 19) ? 1.0 : 0.0;
-        R[2 * node] = 0.0;
-        R[2 * node + 1] = 0.0;
-      } else {
-        double acc[36];
-#pragma unroll
-        for (int e = 0; e < 36; ++e) acc[e] = 0.0;
-        double r0 = F[2 * node], r1 = F[2 * node + 1];
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          // cc: cells (i-1,j-1) a=2, (i,j-1) a=3, (i-1,j) a=1, (i,j) a=0 — same order as k_assemble
-          const int a = (cc == 0) ? 2 : (cc == 1) ? 3 : (cc == 2) ? 1 : 0;
-          const int lc = (i - 1 + (cc & 1) - (i0 - 1)) + (j - 1 + (cc >> 1) - (j0 - 1)) * (kTX + 1);
-#pragma unroll
-          for (int b = 0; b < 4; ++b)
-#pragma unroll
-            for (int k = 0; k < 2; ++k)
-#pragma unroll
-              for (int m = 0; m < 2; ++m) {
-                const int p = 2 * a + k, q = 2 * b + m;
-                const int e = p <= q ? ke_idx(p, q) : ke_idx(q, p);
-                acc[slot_ab(a, b) * 4 + k * 2 + m] += Ks[e * kTC + lc];
-              }
-          r0 += Rs[(2 * a) * kTC + lc];
-          r1 += Rs[(2 * a + 1) * kTC + lc];
-        }
-        R[2 * node] = r0;
-        R[2 * node + 1] = r1;
-        nrm = r0 * r0 + r1 * r1;
-#pragma unroll
-        for (int sl = 0; sl < 9; ++sl) {
-          const int ii = i + (sl % 3) - 1, jj = j + (sl / 3) - 1;
-          const bool bnd = (ii == 0 || ii == n || jj == 0 || jj == n);  // symmetric elimination
-#pragma unroll
-          for (int e = 0; e < 4; ++e) Jst[(long long)(sl * 4 + e) * Nn + node] = bnd ? 0.0 : acc[sl * 4 + e];
-        }
-      }
-    }
-  }
-  const double bs = block_sum(nrm, sh);
-  if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = bs;
-}
-
-// ------------------------------------------------------------------ K1, modal element algebra
-// Same tiling as k_assemble_tiled, with the per-cell algebra reorganised around the structure
-// of the uniform Q1 cell (exact identities, not approximations):
-//  * dN_a/dx(q) = (xi_a + xe_a eta_q)/(2dx), dN_a/dy(q) = (eta_a + xe_a xi_q)/(2dx) with
-//    xe_a = xi_a eta_a, so tau^(N_a e_k)(q) = W_{q,k} mode_a/(2dx), mode_a = (xi_a, eta_a, xe_a),
-//    and every column of W lies in span{p1, p2, p3}:
-//      p1 = (al, be, 0), p2 = (0, 0, be), p3 = (al, -be, 0)   (al = 1/sqrt2, be = 1/(sqrt2 e)).
-//    The element stiffness sum_q w dt tau^_a . C_q tau^_b (eq:linearSVNewton + eq:modification)
-//    is therefore mode_a^T S mode_b with a 6x6 S (15 distinct entries) accumulated from the six
-//    Q_ij = p_i^T C_q p_j = c0 p_i.p_j - c1 (a_i b_j + a_j b_i), a_i = p_i.pi^, b_i = p_i.tau^.
-//  * N_a(q) = phi_a . m_q / 4 with phi_a = (1, xi_a, eta_a, xe_a), m_q = (1, xi_q, eta_q, xi_q eta_q),
-//    so the mass + ocean-drag block sum_q w N_a N_b E_km(q) needs only the four moments
-//    (1, xi_q, eta_q, xi_q eta_q) of E_km:
-//      phi_a^T M phi_b / 16 = [mu0 (1+g2 X_aX_b)(1+g2 Y_aY_b) + mux (X_a+X_b)(1+g2 Y_aY_b)
-//                              + muy (Y_a+Y_b)(1+g2 X_aX_b) + muxy (X_a+X_b)(Y_a+Y_b)] / 16.
-// This cuts the fp64 work per cell ~3x (the tiled kernel is fp64-pipe bound, ncu r01).
-__host__ __device__ constexpr int lidx(int x, int y) { return y ? (x ? 2 : 3) : (x ? 1 : 0); }
-__host__ __device__ constexpr double xe_a(int a) { return xi_a(a) * eta_a(a); }
-__host__ __device__ constexpr double mode_c(int a, int c) { return c == 0 ? xi_a(a) : c == 1 ? eta_a(a) : xe_a(a); }
-
-// Per-step constants of the modal element algebra, computed on the host so the kernel reads
-// them as constant-bank operands (no registers, no device divisions).
-struct ElemK {
-  double al, be, al2, be2, sc, pp11, pp13, pp22, w, wdt, co, dtco, dmin2, prf, hb, dt, inv_dx;
-};
-static ElemK make_elemk(const Phys& ph) {
-  ElemK k;
-  const double inv_dx = 1.0 / ph.dx;
-  k.al = kR2I;
-  k.be = kR2I / ph.e;
-  k.al2 = 2.0 * inv_dx * k.al;
-  k.be2 = 2.0 * inv_dx * k.be;
-  k.w = 0.25 * ph.dx * ph.dx;
-  k.wdt = k.w * ph.dt;
-  k.sc = k.wdt * 0.25 * inv_dx * inv_dx;
-  k.pp11 = k.al * k.al + k.be * k.be;
-  k.pp13 = k.al * k.al - k.be * k.be;
-  k.pp22 = k.be * k.be;
-  k.co = ph.C_o * ph.rho_o;
-  k.dtco = ph.dt * k.co;
-  k.dmin2 = ph.delta_min * ph.delta_min;
-  k.prf = k.wdt * inv_dx;
-  k.hb = 0.5 * k.wdt * inv_dx;
-  k.dt = ph.dt;
-  k.inv_dx = inv_dx;
-  return k;
-}
-
-template <int KIND>
-__device__ __forceinline__ void element_modal(const Phys& ph, const ElemK& K, int ci, int cj, const double* __restrict__ v,
-                                              const double* __restrict__ vo, const double* __restrict__ pi,
-                                              const double* __restrict__ P, const double* __restrict__ rhoh,
-                                              double* __restrict__ Ks, double* __restrict__ Rs, int t) {
-  const int n = ph.n, s = n + 1;
-  const long long Nc = (long long)n * n;
-  const int cell = cj * n + ci;
-  double u[4][2], dw[4][2];  // nodal velocity v and ocean-relative velocity v_o - v
-  {
-    const int nd0 = cj * s + ci;
-    const int ids[4] = {nd0, nd0 + 1, nd0 + s + 1, nd0 + s};
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const double2 a1 = __ldg(reinterpret_cast<const double2*>(v) + ids[b]);
-      const double2 a2 = __ldg(reinterpret_cast<const double2*>(vo) + ids[b]);
-      u[b][0] = a1.x; u[b][1] = a1.y;
-      dw[b][0] = a2.x - a1.x; dw[b][1] = a2.y - a1.y;
-    }
-  }
-  const double Pc = P[cell], rh = rhoh[cell];
-  const double w = K.w, wdt = K.wdt, al = K.al, be = K.be, al2 = K.al2, be2 = K.be2;  // al2 = (2/dx) al
-  const double co = K.co, dmin2 = K.dmin2, sc = K.sc;                                 // sc = w dt/(2dx)^2
-  const double pp11 = K.pp11, pp13 = K.pp13, pp22 = K.pp22;
-  constexpr double g2 = 1.0 / 3.0;
-  // The per-Gauss-point Q_ij and drag coefficients are parked in this thread's 36 Ks slots
-  // (slot 9q + j) and combined after the loop: that keeps the loop's live state small.
-  // The residual is accumulated directly per Gauss point (nodal interpolation, the same
-  // grouping as the per-node residual kernel): it decides Newton convergence at 1e-8, so it
-  // keeps the smallest rounding error rather than the cheapest modal form.
-  double Ra[8];
-#pragma unroll
-  for (int p = 0; p < 8; ++p) Ra[p] = 0.0;
-  // pi of the next Gauss point is fetched one iteration ahead (software pipelining)
-  double pn0 = 0.0, pn1 = 0.0, pn2 = 0.0;
-  if (KIND == SEAICE_JAC_SV) {
-    pn0 = __ldg(pi + cell); pn1 = __ldg(pi + 4 * Nc + cell); pn2 = __ldg(pi + 8 * Nc + cell);
-  }
-#pragma unroll 1
-  for (int q = 0; q < 4; ++q) {
-    const double p11 = pn0, p12 = pn1, p22 = pn2;
-    if (KIND == SEAICE_JAC_SV && q < 3) {
-      pn0 = __ldg(pi + (q + 1) * Nc + cell); pn1 = __ldg(pi + (5 + q) * Nc + cell); pn2 = __ldg(pi + (9 + q) * Nc + cell);
-    }
-    double vx = 0, vy = 0, wx = 0, wy = 0, L00 = 0, L01 = 0, L10 = 0, L11 = 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      vx += Nq(q, b) * u[b][0];
-      vy += Nq(q, b) * u[b][1];
-      wx += Nq(q, b) * dw[b][0];
-      wy += Nq(q, b) * dw[b][1];
-      L00 += Gx(q, b) * u[b][0];
-      L01 += Gy(q, b) * u[b][0];
-      L10 += Gx(q, b) * u[b][1];
-      L11 += Gy(q, b) * u[b][1];
-    }
-    // (Gx, Gy are reference gradients x 2: physical = 0.5 * (2/dx) * G)
-    const double tx = 0.5 * al2 * (L00 + L11), ty = 0.5 * be2 * (L00 - L11), tz = 0.5 * be2 * (L01 + L10);
-    const double X = dmin2 + 2.0 * (tx * tx + ty * ty + tz * tz);  // Delta^2 >= Delta_min^2 > 0
-    const double rD = rsqrt(X);                                      // 1/Delta
-    const double c0 = Pc * rD;
-    const double b1 = al * tx + be * ty, b2 = be * tz, b3 = al * tx - be * ty;
-    const double cs = sc * c0;
-    double Q11 = cs * pp11, Q13 = cs * pp13, Q22 = cs * pp22, Q33 = cs * pp11, Q12 = 0.0, Q23 = 0.0;
-    if (KIND == SEAICE_JAC_SV) {
-      const V3 ph_ = pi_hat(p11, p12, p22);
-      const double a1 = al * ph_.x + be * ph_.y, a2 = be * ph_.z, a3 = al * ph_.x - be * ph_.y;
-      // 1/s = 1/max(1, sqrt2 |pi^|)
-      const double pq = 2.0 * dot3(ph_, ph_);
-      const double isf = pq > 1.0 ? rsqrt(pq) : 1.0;
-      const double c1 = sc * Pc * (rD * rD) * isf;
-      Q11 -= c1 * 2.0 * a1 * b1;
-      Q12 = -c1 * (a1 * b2 + a2 * b1);
-      Q13 -= c1 * (a1 * b3 + a3 * b1);
-      Q22 -= c1 * 2.0 * a2 * b2;
-      Q23 = -c1 * (a2 * b3 + a3 * b2);
-      Q33 -= c1 * 2.0 * a3 * b3;
-    } else if (KIND == SEAICE_JAC_STD) {
-      const double c1 = sc * 2.0 * Pc * (rD * rD * rD);
-      Q11 -= c1 * b1 * b1;
-      Q12 = -c1 * b1 * b2;
-      Q13 -= c1 * b1 * b3;
-      Q22 -= c1 * b2 * b2;
-      Q23 = -c1 * b2 * b3;
-      Q33 -= c1 * b3 * b3;
-    }
-    double* slot = Ks + (9 * q) * kTC + t;
-    slot[0 * kTC] = Q11; slot[1 * kTC] = Q12; slot[2 * kTC] = Q13;
-    slot[3 * kTC] = Q22; slot[4 * kTC] = Q23; slot[5 * kTC] = Q33;
-    // ocean drag linearisation D = C_o rho_o (|w| I + w w^T/|w|), w = v_o - v (eq:A)
-    const double n2 = wx * wx + wy * wy;
-    double nw, inw = 0.0;
-    if (n2 >= 1e-24) {  // |w| >= 1e-12
-      const double r = rsqrt(n2);
-      nw = n2 * r;
-      inw = co * r;
-    } else {
-      nw = sqrt(n2);
-    }
-    const double d00 = co * nw + inw * wx * wx, d11 = co * nw + inw * wy * wy, d01 = inw * wx * wy;
-    slot[6 * kTC] = wdt * d00; slot[7 * kTC] = wdt * d11; slot[8 * kTC] = wdt * d01;
-    // element residual -A(v, phi_{a,k}) (eq:A), term by term as in the per-node kernel
-    const double dtc0 = K.dt * c0, hp = 0.5 * K.dt * Pc, dcn = K.dtco * nw;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const double Na = Nq(q, a), gx = Gx(q, a) * K.inv_dx, gy = Gy(q, a) * K.inv_dx;
-      const double tdx = gx * b1 + gy * b2;  // tau^(v) . tau^(N_a e_x)
-      const double tdy = gy * b3 + gx * b2;  // tau^(v) . tau^(N_a e_y)
-      Ra[2 * a] += -w * (rh * vx * Na + dtc0 * tdx - hp * gx - dcn * wx * Na);
-      Ra[2 * a + 1] += -w * (rh * vy * Na + dtc0 * tdy - hp * gy - dcn * wy * Na);
-    }
-  }
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    Rs[(2 * a) * kTC + t] = Ra[2 * a];
-    Rs[(2 * a + 1) * kTC + t] = Ra[2 * a + 1];
-  }
-  // accumulate S (15 distinct entries) and the drag moments from the parked values
-  double s00 = 0, s01 = 0, s02 = 0, s11 = 0, s12 = 0, s22 = 0, s04 = 0, s05 = 0, s14 = 0, s15 = 0, s24 = 0,
-         s25 = 0, s44 = 0, s45 = 0, s55 = 0;
-  double mx0 = 0, mx1 = 0, mx2 = 0, mx3 = 0, my0 = 0, my1 = 0, my2 = 0, my3 = 0, mc0 = 0, mc1 = 0, mc2 = 0, mc3 = 0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    constexpr double g2c = 1.0 / 3.0;
-    const double xq = xi_q(q), eq = eta_q(q), xe = xq * eq;
-    const double* slot = Ks + (9 * q) * kTC + t;
-    const double Q11 = slot[0], Q12 = slot[1 * kTC], Q13 = slot[2 * kTC], Q22 = slot[3 * kTC],
-                 Q23 = slot[4 * kTC], Q33 = slot[5 * kTC];
-    s00 += Q11; s01 += Q12; s02 += eq * Q11 + xq * Q12;
-    s11 += Q22; s12 += eq * Q12 + xq * Q22; s22 += g2c * (Q11 + Q22) + 2.0 * xe * Q12;
-    s04 += Q13; s05 += eq * Q12 + xq * Q13; s14 += Q23; s15 += eq * Q22 + xq * Q23;
-    s24 += eq * Q13 + xq * Q23; s25 += g2c * (Q12 + Q23) + xe * (Q13 + Q22);
-    s44 += Q33; s45 += eq * Q23 + xq * Q33; s55 += g2c * (Q22 + Q33) + 2.0 * xe * Q23;
-    const double d00 = slot[6 * kTC], d11 = slot[7 * kTC], d01 = slot[8 * kTC];
-    mx0 += d00; mx1 += xq * d00; mx2 += eq * d00; mx3 += xe * d00;
-    my0 += d11; my1 += xq * d11; my2 += eq * d11; my3 += xe * d11;
-    mc0 += d01; mc1 += xq * d01; mc2 += eq * d01; mc3 += xe * d01;
-  }
-  // consistent mass: E_kk += w rh at every Gauss point -> mu0 += 4 w rh
-  mx0 += 4.0 * w * rh;
-  my0 += 4.0 * w * rh;
-  // S blocks (rows/cols 0..2 = x modes, 3..5 = y modes)
-  const double S[6][6] = {{s00, s01, s02, s01, s04, s05}, {s01, s11, s12, s11, s14, s15},
-                          {s02, s12, s22, s12, s24, s25}, {s01, s11, s12, s11, s14, s15},
-                          {s04, s14, s24, s14, s44, s45}, {s05, s15, s25, s15, s45, s55}};
-#pragma unroll
-  for (int qq = 0; qq < 8; ++qq) {
-    const int b = qq >> 1, m = qq & 1;
-    double h[6];
-#pragma unroll
-    for (int r = 0; r < 6; ++r) {
-      double acc = 0.0;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) acc = (mode_c(b, c) > 0) ? acc + S[r][3 * m + c] : acc - S[r][3 * m + c];
-      h[r] = acc;
-    }
-#pragma unroll
-    for (int pp = 0; pp <= qq; ++pp) {
-      const int a = pp >> 1, k = pp & 1;
-      double val = 0.0;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) val = (mode_c(a, c) > 0) ? val + h[3 * k + c] : val - h[3 * k + c];
-      const bool xx = (k == 0 && m == 0), yy = (k == 1 && m == 1);
-      const double mu0 = xx ? mx0 : yy ? my0 : mc0, mu1 = xx ? mx1 : yy ? my1 : mc1;
-      const double mu2 = xx ? mx2 : yy ? my2 : mc2, mu3 = xx ? mx3 : yy ? my3 : mc3;
-      const double XX = xi_a(a) * xi_a(b), YY = eta_a(a) * eta_a(b);
-      const double sx = xi_a(a) + xi_a(b), sy = eta_a(a) + eta_a(b);
-      double md = mu0 * ((1.0 + g2 * XX) * (1.0 + g2 * YY));
-      if (sx != 0.0) md += mu1 * (sx * (1.0 + g2 * YY));
-      if (sy != 0.0) md += mu2 * (sy * (1.0 + g2 * XX));
-      if (sx != 0.0 && sy != 0.0) md += mu3 * (sx * sy);
-      Ks[ke_idx(pp, qq) * kTC + t] = val + 0.0625 * md;
-    }
-  }
-}
-
-template <int KIND>
-__global__ void __launch_bounds__(kTThreads, 2) k_assemble_modal(Phys ph, ElemK K, int Nn, const double* __restrict__ v,
-                                                                 const double* __restrict__ pi,
-                                                                 const double* __restrict__ P,
-                                                                 const double* __restrict__ rhoh,
-                                                                 const double* __restrict__ vo,
-                                                                 const double* __restrict__ F,
-                                                                 double* __restrict__ Jst, double* __restrict__ R,
-                                                                 double* __restrict__ part) {
-  extern __shared__ double smem[];
-  double* Ks = smem;             // [36][kTC]
-  double* Rs = smem + kKE * kTC;  // [8][kTC]
-  __shared__ double sh[32];
-  const int n = ph.n, s = n + 1;
-  const int i0 = blockIdx.x * kTX, j0 = blockIdx.y * kTY;
-  const int t = threadIdx.x;
-  {
-    const int ci = i0 - 1 + t % (kTX + 1), cj = j0 - 1 + t / (kTX + 1);
-    if (ci >= 0 && ci < n && cj >= 0 && cj < n) element_modal<KIND>(ph, K, ci, cj, v, vo, pi, P, rhoh, Ks, Rs, t);
-  }
-  __syncthreads();
-  double nrm = 0.0;
-  if (t < kTX * kTY) {
-    const int i = i0 + t % kTX, j = j0 + t / kTX;
-    if (i <= n && j <= n) {
-      const int node = j * s + i;
-      if (!(i > 0 && i < n && j > 0 && j < n)) {
-#pragma unroll
-        for (int e = 0; e < 36; ++e) Jst[(long long)e * Nn + node] = (e == 16 || e == 19) ? 1.0 : 0.0;
-        R[2 * node] = 0.0;
-        R[2 * node + 1] = 0.0;
-      } else {
-        // cell cc at offset (cc&1, cc>>1) from (i-1, j-1); the node is its local corner (1-ox, 1-oy)
-        const int lc0 = (i - i0) + (j - j0) * (kTX + 1);
-        double r0 = F[2 * node], r1 = F[2 * node + 1];
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const int a = lidx(1 - (cc & 1), 1 - (cc >> 1));
-          const int lc = lc0 + (cc & 1) + (cc >> 1) * (kTX + 1);
-          r0 += Rs[(2 * a) * kTC + lc];
-          r1 += Rs[(2 * a + 1) * kTC + lc];
-        }
-        R[2 * node] = r0;
-        R[2 * node + 1] = r1;
-        nrm = r0 * r0 + r1 * r1;
-#pragma unroll
-        for (int sl = 0; sl < 9; ++sl) {
-          const int dxs = sl % 3 - 1, dys = sl / 3 - 1;
-          const bool bnd = (i + dxs == 0 || i + dxs == n || j + dys == 0 || j + dys == n);  // symmetric elimination
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int k = e >> 1, m = e & 1;
-            double acc = 0.0;
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-              const int ax = 1 - (cc & 1), ay = 1 - (cc >> 1);
-              const int bx = ax + dxs, by = ay + dys;
-              if (bx < 0 || bx > 1 || by < 0 || by > 1) continue;
-              const int p = 2 * lidx(ax, ay) + k, q = 2 * lidx(bx, by) + m;
-              const int lc = lc0 + (cc & 1) + (cc >> 1) * (kTX + 1);
-              acc += Ks[(p <= q ? ke_idx(p, q) : ke_idx(q, p)) * kTC + lc];
-            }
-            Jst[(long long)(sl * 4 + e) * Nn + node] = bnd ? 0.0 : acc;
-          }
-        }
-      }
-    }
-  }
-  const double bs = block_sum(nrm, sh);
-  if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = bs;
-}
-
-// ------------------------------------------------------------------ K1, Hadamard element algebra
-// Same tiling and shared-memory layout as k_assemble_modal; the per-cell arithmetic is cut
-// further with the 4-point Walsh-Hadamard structure of the uniform Q1 cell (exact identities):
+// ------------------------------------------------------------------ K1, fused residual + Jacobian
+// Two-phase, atomics-free: a CTA owns a TX x TY tile of nodes.  Phase 1: one thread per cell of
+// the (TX+1) x (TY+1) cells touching the tile computes the packed 8x8 element matrix (upper
+// triangle, 36 values) and the 8 element residual terms into shared memory (SoA, bank-conflict
+// free).  Phase 2: one thread per node gathers its residual pair and the 19 values of its
+// symmetric stencil row (stencil.cuh) from the four adjacent cells and writes them coalesced.
+// Each cell's quadrature-point algebra is done once per tile (1.16x recompute for the halo at
+// 31 x 8) instead of once per node (4x); every value is written once by one thread.
+//
+// Per-cell algebra: exact identities of the uniform Q1 cell (Walsh-Hadamard structure):
 //  * Phi = [phi_a] (rows phi_a = (1, xi_a, eta_a, xi_a eta_a)) is a signed Hadamard matrix, so a
 //    nodal field f has modal coefficients F^ = Phi^T f (one 8-add butterfly) and
 //      f(q) = (F0 + xi_q F1 + eta_q F2 + xi_q eta_q F3)/4,  df/dx = (F1 + eta F3)/(2dx),
 //      df/dy = (F2 + xi F3)/(2dx):  tau^(v)(q) is affine in (xi_q, eta_q) with 7 coefficients.
+//  * tau^(N_a e_k)(q) = W_{q,k} mode_a/(2dx), mode_a = (xi_a, eta_a, xi_a eta_a), with the columns
+//    of W in span{p1, p2, p3}: p1 = (al, be, 0), p2 = (0, 0, be), p3 = (al, -be, 0)
+//    (al = 1/sqrt2, be = 1/(sqrt2 e)), so the viscous element stiffness
+//    sum_q w dt tau^_a . C_q tau^_b (eq:linearSVNewton + eq:modification) is mode_a^T S^km mode_b
+//    with S built from the six Q_ij = p_i^T C_q p_j = c0 p_i.p_j - c1 (a_i b_j + a_j b_i),
+//    a_i = p_i.pi^, b_i = p_i.tau^.
 //  * The per-Gauss-point Q_ij and drag values are parked (9 per q) and reduced to their four
 //    q-moments (sum, xi-, eta-, xi*eta-weighted) by the same butterfly.
 //  * Each 4x4 component block of the element matrix is E^km = Phi M^km Phi^T with
 //      M^km = (1/16) sum_q E_km(q) m_q m_q^T  (mass + ocean drag, m_q = (1, xi_q, eta_q, xi_q eta_q))
-//             + [0, 0; 0, S^km]                (viscous stiffness, S of k_assemble_modal),
-//    i.e. one 2-D 4x4 Walsh-Hadamard transform per block instead of a per-entry expansion.
+//             + [0, 0; 0, S^km]                (viscous stiffness),
+//    i.e. one 2-D 4x4 Walsh-Hadamard transform per block.
 //  * The element residual stays in per-Gauss-point nodal form (it decides Newton convergence at
-//    1e-8, see k_assemble_modal), with the factors -w, dt, 1/dx folded into 5 per-q coefficients.
+//    1e-8: a moment form raised the rounding floor), with -w, dt, 1/dx folded into 5 per-q
+//    coefficients.
+constexpr int kKE = 36;
+__host__ __device__ constexpr int ke_idx(int p, int q) { return p * 8 - p * (p - 1) / 2 + (q - p); }  // p <= q
+__host__ __device__ constexpr int lidx(int x, int y) { return y ? (x ? 2 : 3) : (x ? 1 : 0); }
+
 struct ElemH {
   double ka, kb;              // al/(2dx), be/(2dx): tau^ coefficients from unscaled modal gradients
   double al, be;              // 1/sqrt2, 1/(sqrt2 e)
@@ -1300,9 +772,9 @@ __device__ __forceinline__ double gather_node_rows(int n, int Nn, int i0, int j0
                                                    double* __restrict__ R) {
   const int s = n + 1;
   const int node = j * s + i;
-  if (!(i > 0 && i < n && j > 0 && j < n)) {
+  if (!(i > 0 && i < n && j > 0 && j < n)) {  // Dirichlet row: identity
 #pragma unroll
-    for (int e = 0; e < 36; ++e) Jst[(long long)e * Nn + node] = (e == 16 || e == 19) ? 1.0 : 0.0;
+    for (int e = 0; e < kJS; ++e) Jst[(long long)e * Nn + node] = (e == kJDxx || e == kJDyy) ? 1.0 : 0.0;
     R[2 * node] = 0.0;
     R[2 * node + 1] = 0.0;
     return 0.0;
@@ -1319,12 +791,14 @@ __device__ __forceinline__ double gather_node_rows(int n, int Nn, int i0, int j0
   }
   R[2 * node] = r0;
   R[2 * node + 1] = r1;
+  // stencil slots 4 (own block: xx, xy, yy) and 5..8 (E, NW, N, NE: full 2x2 blocks)
 #pragma unroll
-  for (int sl = 0; sl < 9; ++sl) {
+  for (int sl = 4; sl < 9; ++sl) {
     const int dxs = sl % 3 - 1, dys = sl / 3 - 1;
     const bool bnd = (i + dxs == 0 || i + dxs == n || j + dys == 0 || j + dys == n);  // symmetric elimination
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
+      if (sl == 4 && e == 2) continue;  // J_yx = J_xy
       const int k = e >> 1, m = e & 1;
       double acc = 0.0;
       bool first = true;
@@ -1339,7 +813,8 @@ __device__ __forceinline__ double gather_node_rows(int n, int Nn, int i0, int j0
         acc = first ? val : acc + val;  // no 0.0 + x (not foldable under IEEE signed zeros)
         first = false;
       }
-      Jst[(long long)(sl * 4 + e) * Nn + node] = bnd ? 0.0 : acc;
+      const int dst = sl == 4 ? kJDxx + (e == 3 ? 2 : e) : (sl - 5) * 4 + e;
+      Jst[(long long)dst * Nn + node] = bnd ? 0.0 : acc;
     }
   }
   return r0 * r0 + r1 * r1;
@@ -1427,7 +902,7 @@ static int launch_assemble_had_t(Ctx& c, const double* v, const double* pi, doub
                                                              c.rhoh.get(), c.vocean.get(), c.F.get(), c.Jst.get(), R,
                                                              c.part.get());
   SI_LAUNCHED(c);
-  prof_end(c, PC_ASSEMBLE, 352.0 * c.Nn + 112.0 * c.Nc);
+  prof_end(c, PC_ASSEMBLE, kAsmBytesNode * c.Nn + 112.0 * c.Nc);
   return g;
 }
 
@@ -1438,55 +913,13 @@ static int launch_assemble_had(Ctx& c, const double* v, const double* pi, double
   return launch_assemble_had_t<KIND, 31, 8>(c, v, pi, R);
 }
 
-template <int KIND>
-static int launch_assemble_modal(Ctx& c, const double* v, const double* pi, double* R) {
-  static bool attr = false;
-  if (!attr) {
-    SI_CUDA(cudaFuncSetAttribute(k_assemble_modal<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kTileSmem));
-    attr = true;
-  }
-  const dim3 grid((c.n + 1 + kTX - 1) / kTX, (c.n + 1 + kTY - 1) / kTY);
-  const int g = grid.x * grid.y;
-  c.part.ensure(c.al, g + 64);
-  prof_begin(c);
-  k_assemble_modal<KIND><<<grid, kTThreads, kTileSmem, c.s>>>(c.ph, make_elemk(c.ph), c.Nn, v, pi, c.P.get(), c.rhoh.get(),
-                                                               c.vocean.get(), c.F.get(), c.Jst.get(), R,
-                                                               c.part.get());
-  SI_LAUNCHED(c);
-  prof_end(c, PC_ASSEMBLE, 352.0 * c.Nn + 112.0 * c.Nc);
-  return g;
-}
-
-template <int KIND>
-static int launch_assemble_tiled(Ctx& c, const double* v, const double* pi, double* R) {
-  static bool attr = false;
-  if (!attr) {
-    SI_CUDA(cudaFuncSetAttribute(k_assemble_tiled<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kTileSmem));
-    attr = true;
-  }
-  const dim3 grid((c.n + 1 + kTX - 1) / kTX, (c.n + 1 + kTY - 1) / kTY);
-  const int g = grid.x * grid.y;
-  c.part.ensure(c.al, g + 64);
-  prof_begin(c);
-  k_assemble_tiled<KIND><<<grid, kTThreads, kTileSmem, c.s>>>(c.ph, c.Nn, v, pi, c.P.get(), c.rhoh.get(),
-                                                               c.vocean.get(), c.F.get(), c.Jst.get(), R,
-                                                               c.part.get());
-  SI_LAUNCHED(c);
-  prof_end(c, PC_ASSEMBLE, 352.0 * c.Nn + 112.0 * c.Nc);
-  return g;
-}
-
-template <int KIND, bool JAC>
-static void launch_assemble(Ctx& c, const double* v, const double* pi, double* R) {
+static void launch_residual(Ctx& c, const double* v, double* R) {
   const int g = grid_for(c.Nn, 128);
   c.part.ensure(c.al, g + 64);
   prof_begin(c);
-  k_assemble<KIND, JAC><<<g, 128, 0, c.s>>>(c.ph, c.Nn, v, pi, c.P.get(), c.rhoh.get(), c.vocean.get(), c.F.get(),
-                                             c.Jst.get(), R, c.part.get());
+  k_residual<<<g, 128, 0, c.s>>>(c.ph, c.Nn, v, c.P.get(), c.rhoh.get(), c.vocean.get(), c.F.get(), R, c.part.get());
   SI_LAUNCHED(c);
-  prof_end(c, PC_ASSEMBLE, JAC ? 352.0 * c.Nn + 112.0 * c.Nc : 64.0 * c.Nn + 16.0 * c.Nc);
+  prof_end(c, PC_ASSEMBLE, 64.0 * c.Nn + 16.0 * c.Nc);
 }
 
 void assemble_impl(Ctx& c, const double* v, const double* pi, bool jac, double* r_out, double* norm_host) {
@@ -1497,15 +930,7 @@ void assemble_impl(Ctx& c, const double* v, const double* pi, bool jac, double* 
   const int kind = c.p.jacobian;
   int nparts = grid_for(c.Nn, 128);
   if (!jac) {
-    launch_assemble<SEAICE_JAC_PICARD, false>(c, v, pp, R);  // residual only: per-node gather
-  } else if (getenv("SEAICE_ASM_OLD")) {
-    if (kind == SEAICE_JAC_SV) nparts = launch_assemble_tiled<SEAICE_JAC_SV>(c, v, pp, R);
-    else if (kind == SEAICE_JAC_STD) nparts = launch_assemble_tiled<SEAICE_JAC_STD>(c, v, pp, R);
-    else nparts = launch_assemble_tiled<SEAICE_JAC_PICARD>(c, v, pp, R);
-  } else if (getenv("SEAICE_ASM_MODAL")) {
-    if (kind == SEAICE_JAC_SV) nparts = launch_assemble_modal<SEAICE_JAC_SV>(c, v, pp, R);
-    else if (kind == SEAICE_JAC_STD) nparts = launch_assemble_modal<SEAICE_JAC_STD>(c, v, pp, R);
-    else nparts = launch_assemble_modal<SEAICE_JAC_PICARD>(c, v, pp, R);
+    launch_residual(c, v, R);  // residual only: per-node gather
   } else if (kind == SEAICE_JAC_SV) {
     nparts = launch_assemble_had<SEAICE_JAC_SV>(c, v, pp, R);
   } else if (kind == SEAICE_JAC_STD) {

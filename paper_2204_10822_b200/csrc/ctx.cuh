@@ -131,8 +131,8 @@ struct Ctx {
   bool have_load = false;
   DBuf<int> flag;  // validation / misc device flags
 
-  // finest-level Jacobian: 3x3 node stencil of 2x2 blocks, slot-major SoA
-  //   Jst[(s*4 + k*2 + m)*Nn + node], s = (dj+1)*3 + (di+1)
+  // finest-level Jacobian: upper half of the symmetric 3x3 node stencil of 2x2 blocks,
+  // 19 values per node, slot-major SoA (layout in stencil.cuh)
   DBuf<double> Jst;
   DBuf<double> R;  // residual of the last assemble
   double last_res_norm = 0.0;

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "ctx.cuh"
+#include "stencil.cuh"
 
 namespace seaice {
 
@@ -15,9 +16,9 @@ __global__ void k_point_jacobi(int Nn, const double* __restrict__ J, const doubl
                                double* __restrict__ z) {
   const int node = blockIdx.x * blockDim.x + threadIdx.x;
   if (node >= Nn) return;
-  // diagonal entries of the centre block: slot 4, (0,0) and (1,1)
-  z[2 * node] = r[2 * node] / J[16LL * Nn + node];
-  z[2 * node + 1] = r[2 * node + 1] / J[19LL * Nn + node];
+  // diagonal entries of the node's own block
+  z[2 * node] = r[2 * node] / J[(long long)kJDxx * Nn + node];
+  z[2 * node + 1] = r[2 * node + 1] / J[(long long)kJDyy * Nn + node];
 }
 
 void precond_apply(Ctx& c, const double* r, double* z) {

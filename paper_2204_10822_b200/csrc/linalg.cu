@@ -5,35 +5,27 @@
 #include <cstring>
 
 #include "ctx.cuh"
+#include "stencil.cuh"
 
 namespace seaice {
 
 // ------------------------------------------------------------------ stencil SpMV
-// y = J x with J stored as 9 slots of 2x2 blocks per node, slot-major SoA: every load
-// of J is coalesced and no index is read (8 B per stored value).  x is read as double2
-// per neighbour node; the 3 node lines a warp touches stay in L1/L2.
+// y = J x with J in the symmetric 19-value slot-major SoA storage of stencil.cuh: every load of
+// J is coalesced and no index is read.  x is read as double2 per neighbour node; the 3 node
+// lines a warp touches stay in L1/L2, and the lower-neighbour blocks (one node line below) are
+// L2 hits, so J crosses HBM once (152 B per node).
 __global__ void __launch_bounds__(256) k_stencil_spmv(int n, int Nn, const double* __restrict__ J,
                                                       const double2* __restrict__ x, double2* __restrict__ y) {
   const int node = blockIdx.x * blockDim.x + threadIdx.x;
   if (node >= Nn) return;
   const int s = n + 1, i = node % s, j = node / s;
-  double y0 = 0.0, y1 = 0.0;
   if (i > 0 && i < n && j > 0 && j < n) {
-#pragma unroll
-    for (int sl = 0; sl < 9; ++sl) {
-      const int nb = node + (sl / 3 - 1) * s + (sl % 3 - 1);
-      const double2 xv = __ldg(x + nb);
-      const double* Js = J + (long long)sl * 4 * Nn + node;
-      y0 += __ldg(Js) * xv.x + __ldg(Js + Nn) * xv.y;
-      y1 += __ldg(Js + 2 * (long long)Nn) * xv.x + __ldg(Js + 3 * (long long)Nn) * xv.y;
-    }
+    y[node] = stencil_apply(J, Nn, s, node, x);
   } else {
     const double2 xv = x[node];
-    const double* Js = J + 16LL * Nn + node;
-    y0 = Js[0] * xv.x + Js[Nn] * xv.y;
-    y1 = Js[2LL * Nn] * xv.x + Js[3LL * Nn] * xv.y;
+    const double4 D = stencil_diag(J, Nn, node);
+    y[node] = make_double2(D.x * xv.x + D.y * xv.y, D.z * xv.x + D.w * xv.y);
   }
-  y[node] = make_double2(y0, y1);
 }
 
 void stencil_spmv(Ctx& c, const double* x, double* y) {
@@ -41,7 +33,7 @@ void stencil_spmv(Ctx& c, const double* x, double* y) {
   k_stencil_spmv<<<grid_for(c.Nn), 256, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), reinterpret_cast<const double2*>(x),
                                                   reinterpret_cast<double2*>(y));
   SI_LAUNCHED(c);
-  prof_end(c, PC_SPMV0, 320.0 * c.Nn);
+  prof_end(c, PC_SPMV0, kSpmvBytesNode * c.Nn);
 }
 
 // ------------------------------------------------------------------ BSR SpMV

@@ -1431,7 +1431,10 @@ __global__ void __launch_bounds__(256) k_gspmv(int nb, const int* __restrict__ r
   else if (SR > BR && row < nb && lig == BR) y[i] = 0.0;
 }
 
-// fused Chebyshev step (same semantics as k_cheb_stencil) on a coarse level (padded vectors)
+// fused Chebyshev step (same semantics as k_cheb_stencil) on a coarse level (padded vectors).
+// Lane a < B of a group owns component a of the block row (its vector loads are issued before
+// the row loop; one instruction serves a whole group), lane B writes the pad entries, and the
+// D^-1 r product gathers r from the group's lanes by shuffles.
 template <int B, int G>
 __global__ void __launch_bounds__(256) k_gcheb(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
                                                const double* __restrict__ val, const double* __restrict__ dinv,
@@ -1441,36 +1444,34 @@ __global__ void __launch_bounds__(256) k_gcheb(int nb, const int* __restrict__ r
   constexpr int S = vstride(B);
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int row = (int)(t / G), lig = (int)(t % G);
+  const bool own = row < nb && lig < B;
+  const bool pad = S > B && row < nb && lig == B;
+  const long long i = (long long)row * S + lig;
+  double dv = 0.0, xv = 0.0, rv = 0.0, D[B];
+#pragma unroll
+  for (int k = 0; k < B; ++k) D[k] = 0.0;
+  if (own) {
+    dv = d[i];
+    if (!first) xv = x[i];
+    if (want_r) rv = r[i];
+    if (want_d) {
+#pragma unroll
+      for (int k = 0; k < B; ++k) D[k] = __ldg(dinv + (long long)row * B * B + lig * B + k);
+    }
+  }
   double acc[B];
   if (want_r) grp_row<B, B, G>(row, nb, lig, rp, ci, val, d, acc);
-  if (row >= nb || lig != 0) return;
-  double dv[B];
+  if (own) x[i] = xv + dv;
+  else if (pad && first) x[i] = 0.0;
+  if (!want_r) return;  // uniform across the launch
+  rv -= own ? pick<B>(acc, lig) : 0.0;
+  if (own) r[i] = rv;
+  if (!want_d) return;
+  double z = 0.0;
 #pragma unroll
-  for (int a = 0; a < B; ++a) {
-    const long long i = (long long)row * S + a;
-    dv[a] = d[i];
-    x[i] = (first ? 0.0 : x[i]) + dv[a];
-  }
-  if (S > B && first) x[(long long)row * S + B] = 0.0;
-  if (!want_r) return;
-  double rv[B];
-#pragma unroll
-  for (int a = 0; a < B; ++a) {
-    const long long i = (long long)row * S + a;
-    rv[a] = r[i] - acc[a];
-    r[i] = rv[a];
-  }
-  if (want_d) {
-    const double* D = dinv + (long long)row * B * B;
-#pragma unroll
-    for (int a = 0; a < B; ++a) {
-      double z = 0.0;
-#pragma unroll
-      for (int b = 0; b < B; ++b) z += D[a * B + b] * rv[b];
-      dout[(long long)row * S + a] = c1 * dv[a] + c2 * z;
-    }
-    if (S > B) dout[(long long)row * S + B] = 0.0;
-  }
+  for (int k = 0; k < B; ++k) z += D[k] * __shfl_sync(0xffffffffu, rv, k, G);
+  if (own) dout[i] = c1 * dv + c2 * z;
+  else if (pad) dout[i] = 0.0;
 }
 
 // r = b - A x (x may be NULL: r = b); d = c2 Dinv r (padded vectors)

@@ -256,8 +256,8 @@ void xpby(Ctx& c, const double* x, double b, double* y, long long n);   // y = x
 void fill(Ctx& c, double* y, double v, long long n);
 void copy(Ctx& c, double* dst, const double* src, long long n);
 // FGMRES helpers: h[0..j] = V[0..j]^T w ; w -= V h, return ||w||
-void multidot(Ctx& c, const double* V, long long ld, int k, const double* w, long long n, double* h_host);
-double multi_axpy_norm(Ctx& c, const double* V, long long ld, int k, const double* h_host, double* w, long long n);
+// h = V[:, :k]^T w, w -= V h, vnext = w / ||w||; returns ||w|| (one host sync)
+double arnoldi_step(Ctx& c, const double* V, long long ld, int k, double* w, long long n, double* vnext, double* h_host);
 void multi_axpy(Ctx& c, const double* Z, long long ld, int k, const double* y_host, double* x, long long n);
 
 // krylov.cu

@@ -73,12 +73,10 @@ int fgmres_impl(Ctx& c, const double* b, double* x, seaice_krylov_stats* st) {
       double* zj = Z + (long long)j * N;
       precond_apply(c, vj, zj);
       apply_A(c, zj, w);
-      multidot(c, V, N, j + 1, w, N, h.data());
-      const double hn = multi_axpy_norm(c, V, N, j + 1, h.data(), w, N);
+      const double hn = arnoldi_step(c, V, N, j + 1, w, N, V + (long long)(j + 1) * N, h.data());
       SI_CHECK(std::isfinite(hn), SEAICE_ENONFINITE, "fgmres: non-finite Arnoldi vector");
       for (int i = 0; i <= j; ++i) H[i * m + j] = h[i];
       H[(j + 1) * m + j] = hn;
-      if (hn > 0.0) scal_copy(c, 1.0 / hn, w, V + (long long)(j + 1) * N, N);
       for (int i = 0; i < j; ++i) {
         const double t = cs[i] * H[i * m + j] + sn[i] * H[(i + 1) * m + j];
         H[(i + 1) * m + j] = -sn[i] * H[i * m + j] + cs[i] * H[(i + 1) * m + j];

@@ -161,73 +161,112 @@ double dot(Ctx& c, const double* a, const double* b, long long n) {
 }
 double norm2(Ctx& c, const double* a, long long n) { return std::sqrt(dot(c, a, a, n)); }
 
-// h[i] = V_i . w for i < k (classical Gram-Schmidt projections), chunks of 8 vectors.
-template <int CH>
-__global__ void __launch_bounds__(256) k_multidot(long long n, const double* __restrict__ V, long long ld, int k0,
-                                                  int k, const double* __restrict__ w, double* __restrict__ part) {
-  __shared__ double sh[32];
-  double acc[CH];
+// h[i] = V_i . w for i < k (classical Gram-Schmidt projections).  One launch: block row y owns
+// vectors [8y, 8y + 8) (8 accumulators per thread keep the occupancy high), each thread 2
+// consecutive entries (16-byte loads); partial sums combined warp-wise, then across the block's
+// warps in a fixed order (deterministic).
+constexpr int kMDT = 256, kMDC = 8;
+__global__ void __launch_bounds__(kMDT) k_multidot(long long n2, const double2* __restrict__ V, long long ld2, int k,
+                                                   const double2* __restrict__ w, double* __restrict__ part) {
+  __shared__ double sh[kMDT / 32][kMDC];
+  const int k0 = blockIdx.y * kMDC;
+  double acc[kMDC];
 #pragma unroll
-  for (int t = 0; t < CH; ++t) acc[t] = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const double wi = w[i];
+  for (int t = 0; t < kMDC; ++t) acc[t] = 0.0;
+  for (long long i = blockIdx.x * (long long)kMDT + threadIdx.x; i < n2; i += (long long)gridDim.x * kMDT) {
+    const double2 wi = w[i];
 #pragma unroll
-    for (int t = 0; t < CH; ++t)
-      if (k0 + t < k) acc[t] += V[(long long)(k0 + t) * ld + i] * wi;
+    for (int t = 0; t < kMDC; ++t)
+      if (k0 + t < k) {
+        const double2 v = __ldg(V + (k0 + t) * ld2 + i);
+        acc[t] += v.x * wi.x + v.y * wi.y;
+      }
   }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-  for (int t = 0; t < CH; ++t) {
-    if (k0 + t < k) {
-      const double s = block_sum(acc[t], sh);
-      if (threadIdx.x == 0) part[(long long)(k0 + t) * gridDim.x + blockIdx.x] = s;
-    }
+  for (int t = 0; t < kMDC; ++t) {
+    const double v = warp_sum(acc[t]);
+    if (lane == 0) sh[wid][t] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kMDC && k0 + threadIdx.x < k) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < kMDT / 32; ++q) s += sh[q][threadIdx.x];
+    part[(long long)(k0 + threadIdx.x) * gridDim.x + blockIdx.x] = s;
   }
 }
 
-void multidot(Ctx& c, const double* V, long long ld, int k, const double* w, long long n, double* h_host) {
-  const int g = red_grid(n);
-  c.part.ensure(c.al, (size_t)g * (k + 8));
-  prof_begin(c);
-  for (int k0 = 0; k0 < k; k0 += 8) {
-    k_multidot<8><<<g, 256, 0, c.s>>>(n, V, ld, k0, k, w, c.part.get());
-    SI_LAUNCHED(c);
-  }
-  prof_end(c, PC_MDOT, 8.0 * (k + 1) * n);
-  finish_cols(c, g, k, h_host);
-}
-
-// w -= sum_i h_i V_i, then partial ||w||^2.
-__global__ void __launch_bounds__(256) k_multi_axpy_norm(long long n, const double* __restrict__ V, long long ld, int k,
-                                                         const double* __restrict__ h, double* __restrict__ w,
-                                                         double* __restrict__ part) {
+// w -= sum_i h_i V_i, then partial ||w||^2 (2 entries per thread, 16-byte loads).
+__global__ void __launch_bounds__(256) k_multi_axpy_norm(long long n2, const double2* __restrict__ V, long long ld2,
+                                                         int k, const double* __restrict__ h,
+                                                         double2* __restrict__ w, double* __restrict__ part) {
   __shared__ double sh[32];
   __shared__ double hs[64];
   if (threadIdx.x < k) hs[threadIdx.x] = h[threadIdx.x];
   __syncthreads();
   double s = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    double wi = w[i];
-    for (int t = 0; t < k; ++t) wi -= hs[t] * V[(long long)t * ld + i];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+    double2 wi = w[i];
+    int t = 0;
+    for (; t + 4 <= k; t += 4) {
+      const double2 a0 = __ldg(V + t * ld2 + i), a1 = __ldg(V + (t + 1) * ld2 + i);
+      const double2 a2 = __ldg(V + (t + 2) * ld2 + i), a3 = __ldg(V + (t + 3) * ld2 + i);
+      wi.x -= hs[t] * a0.x; wi.y -= hs[t] * a0.y;
+      wi.x -= hs[t + 1] * a1.x; wi.y -= hs[t + 1] * a1.y;
+      wi.x -= hs[t + 2] * a2.x; wi.y -= hs[t + 2] * a2.y;
+      wi.x -= hs[t + 3] * a3.x; wi.y -= hs[t + 3] * a3.y;
+    }
+    for (; t < k; ++t) {
+      const double2 a0 = __ldg(V + t * ld2 + i);
+      wi.x -= hs[t] * a0.x; wi.y -= hs[t] * a0.y;
+    }
     w[i] = wi;
-    s += wi * wi;
+    s += wi.x * wi.x + wi.y * wi.y;
   }
   s = block_sum(s, sh);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-double multi_axpy_norm(Ctx& c, const double* V, long long ld, int k, const double* h_host, double* w, long long n) {
-  SI_CHECK(k <= 64, SEAICE_EINVAL, "multi_axpy: k > 64");
-  const int g = red_grid(n);
-  c.part.ensure(c.al, (size_t)g * 40);
-  // pageable source: the runtime stages it before returning, so h_host may be reused at once
-  SI_CUDA(cudaMemcpyAsync(c.scal.get() + 64, h_host, sizeof(double) * k, cudaMemcpyHostToDevice, c.s));
+// One Arnoldi orthogonalisation step with a single host synchronisation: h = V^T w (device),
+// w -= V h, ||w|| (device), v_{k} = w / ||w|| (device), then h and ||w||^2 are copied to the host
+// together.  (The previous form round-tripped h through the host before the update.)
+__global__ void k_normalize(long long n, const double* __restrict__ w, const double* __restrict__ nrm2,
+                            double* __restrict__ out) {
+  const double s2 = *nrm2;
+  const double a = s2 > 0.0 ? 1.0 / sqrt(s2) : 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = a * w[i];
+}
+
+double arnoldi_step(Ctx& c, const double* V, long long ld, int k, double* w, long long n, double* vnext,
+                    double* h_host) {
+  SI_CHECK(n % 2 == 0 && ld % 2 == 0, SEAICE_EINVAL, "arnoldi: odd length");
+  SI_CHECK(k <= 64, SEAICE_EINVAL, "arnoldi: k > 64");
+  const int g = red_grid(n / 2);
+  c.part.ensure(c.al, (size_t)g * (k + 8));
+  double* hd = c.scal.get() + 64;   // h (k values)
+  double* n2d = c.scal.get() + 200;  // ||w||^2
+  const double2* V2 = reinterpret_cast<const double2*>(V);
   prof_begin(c);
-  k_multi_axpy_norm<<<g, 256, 0, c.s>>>(n, V, ld, k, c.scal.get() + 64, w, c.part.get());
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  k_multidot<<<dim3(g, (k + kMDC - 1) / kMDC), kMDT, 0, c.s>>>(n / 2, V2, ld / 2, k, w2, c.part.get());
+  SI_LAUNCHED(c);
+  prof_end(c, PC_MDOT, 8.0 * (k + 1) * n);
+  k_sum_cols<<<1, 1024, 0, c.s>>>(c.part.get(), g, k, hd);
+  SI_LAUNCHED(c);
+  prof_begin(c);
+  k_multi_axpy_norm<<<g, 256, 0, c.s>>>(n / 2, V2, ld / 2, k, hd, reinterpret_cast<double2*>(w), c.part.get());
   SI_LAUNCHED(c);
   prof_end(c, PC_MAXPY_NORM, 8.0 * (k + 2) * n);
-  double r;
-  finish_cols(c, g, 1, &r);
-  return std::sqrt(r);
+  k_sum_cols<<<1, 1024, 0, c.s>>>(c.part.get(), g, 1, n2d);
+  k_normalize<<<vgrid(n), kThreads, 0, c.s>>>(n, w, n2d, vnext);
+  SI_LAUNCHED(c);
+  SI_CUDA(cudaMemcpyAsync(c.hbuf, hd, sizeof(double) * k, cudaMemcpyDeviceToHost, c.s));
+  SI_CUDA(cudaMemcpyAsync(c.hbuf + 128, n2d, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+  SI_CUDA(cudaStreamSynchronize(c.s));
+  std::memcpy(h_host, c.hbuf, sizeof(double) * k);
+  return std::sqrt(c.hbuf[128]);
 }
 
 // x += sum_i y_i Z_i

@@ -76,3 +76,13 @@ x, st, rc = ctx.fgmres(R)
 torch.cuda.synchronize()
 dt = time.time() - t0
 print(f"FGMRES: {st['iters']} its, {1e3*dt:.1f} ms, {1e3*dt/max(st['iters'],1):.3f} ms/it")
+ctx.profile(True)
+x, st, rc = ctx.fgmres(R)
+p = ctx.profile_read()
+ctx.profile(False)
+print(f"FGMRES profiled (eager V-cycle): {st['iters']} its")
+for k, d in p.items():
+    if d["launches"]:
+        print(f"  {k:14s} {d['ms']/st['iters']*1e3:9.1f} us/it  {d['launches']/st['iters']:5.1f} launches/it  "
+              f"{d['bytes']/max(d['ms'],1e-9)/1e6:8.1f} GB/s")
+

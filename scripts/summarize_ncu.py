@@ -17,7 +17,7 @@ TAG = sys.argv[1] if len(sys.argv) > 1 else "r01"
 CLASS = [("k_chebM_stencil", "cheb0_fused"), ("k_cheb_stencil", "cheb0"), ("k_gcheb", "cheb_coarse"),
          ("k_gresid", "resid_coarse"), ("k_gspmv", "transfer"), ("k_resid_dinv_stencil", "resid0"),
          ("k_dense_gemv", "coarse_solve"), ("k_stencil_spmv", "spmv0"), ("k_multidot", "multidot"),
-         ("k_multi_axpy_norm", "maxpy_norm"), ("k_assemble_modal", "assemble"), ("k_delta_energy", "delta_energy")]
+         ("k_multi_axpy_norm", "maxpy_norm"), ("k_assemble_had", "assemble"), ("k_delta_energy", "delta_energy")]
 
 
 def klass(name):

@@ -163,6 +163,17 @@ int seaice_assemble_jacobian(seaice_ctx* ctx, const double* v, const double* pi,
 /* y = J x with the last assembled Jacobian. */
 int seaice_spmv(seaice_ctx* ctx, const double* x, double* y);
 
+/* Explicit transport of A and H between momentum steps: one explicit-Euler,
+ * first-order upwind finite-volume step of eq:model:A / eq:model:H ("an explicit
+ * time step (e.g., an explicit Euler step)"; scheme = DESIGN.md reading G28).
+ * v: nodal velocity [2(n+1)^2] interleaved (device); A, H: cell fields [n*n] row-major
+ * (device, read); A_out, H_out: [n*n] (device, written; must not alias A or H).  Face-normal
+ * velocity = mean of the face's two nodal velocities; an inflow boundary face carries A_in /
+ * H_in; A_out is clamped to [0,1], H_out to [0,inf).  Enqueued on the ctx stream,
+ * no synchronisation.  EINVAL on NULL / aliased buffers or dt < 0 / non-finite. */
+int seaice_transport(seaice_ctx* ctx, double dt, const double* v, const double* A, const double* H,
+                     double A_in, double H_in, double* A_out, double* H_out);
+
 /* Build the AMG hierarchy of the last assembled Jacobian on the GPU: node-block
  * strength, MIS(2) aggregation, rigid-body tentative prolongator, smoothed
  * prolongator, Galerkin R A P via SpGEMM, block-Jacobi Chebyshev data, dense

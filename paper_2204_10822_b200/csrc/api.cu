@@ -339,6 +339,14 @@ int seaice_spmv(seaice_ctx* h, const double* x, double* y) {
   API_END
 }
 
+int seaice_transport(seaice_ctx* h, double dt, const double* v, const double* A, const double* H, double A_in,
+                     double H_in, double* A_out, double* H_out) {
+  API_BEGIN(h)
+  transport_impl(c, dt, v, A, H, A_in, H_in, A_out, H_out);
+  return SEAICE_OK;
+  API_END
+}
+
 int seaice_amg_setup(seaice_ctx* h, int32_t* levels_out, double* oc_out) {
   API_BEGIN(h)
   SI_CHECK(c.assembled, SEAICE_ESTATE, "amg_setup before assemble_jacobian");

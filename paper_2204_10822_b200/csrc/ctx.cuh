@@ -1,5 +1,6 @@
 // ctx.cuh — the library context and the host-side entry points of every kernel family.
 #pragma once
+#include <cmath>
 #include <string>
 #include <vector>
 
@@ -96,6 +97,7 @@ enum ProfClass {
   PC_RESIDC = 11,   // residual + Dinv, coarse levels
   PC_PIUPD = 12,    // K12 dual update
   PC_CHEB0F = 13,   // K4 three Chebyshev steps fused (temporal blocking), finest level
+  PC_TRANSPORT = 14,  // NEXT-3 explicit upwind transport of A, h
   PC_NCLASS = 16
 };
 struct Prof {
@@ -239,6 +241,8 @@ inline void prof_end(Ctx& c, int k, double bytes = 0.0) {
 void set_step_impl(Ctx& c, double dt, double t_new, const double* h, const double* A, const double* v_prev,
                    const double* v_air, const double* v_ocean, const double* load);
 void assemble_impl(Ctx& c, const double* v, const double* pi, bool jacobian, double* r_out, double* norm_host);
+void transport_impl(Ctx& c, double dt, const double* v, const double* A, const double* H, double A_in, double H_in,
+                    double* Ao, double* Ho);
 void build_csr_view(Ctx& c, seaice_csr* out);
 void delta_energy_impl(Ctx& c, const double* v, const double* vt, const double* alphas, int count, double* out,
                        double* sabs = nullptr);

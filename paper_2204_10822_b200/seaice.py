@@ -123,6 +123,7 @@ def lib(build_if_missing: bool = True):
             "seaice_residual": (C.c_int, [VP, VP, VP, P(D)]),
             "seaice_assemble_jacobian": (C.c_int, [VP, VP, VP, P(CSR)]),
             "seaice_spmv": (C.c_int, [VP, VP, VP]),
+            "seaice_transport": (C.c_int, [VP, D, VP, VP, VP, D, D, VP, VP]),
             "seaice_amg_setup": (C.c_int, [VP, P(I32), P(D)]),
             "seaice_amg_level": (C.c_int, [VP, I32, P(BSR), P(BSR), VP]),
             "seaice_precond_apply": (C.c_int, [VP, VP, VP]),
@@ -259,7 +260,7 @@ class SeaIce:
         return int(self.L.seaice_launch_count(self.h))
 
     PROF_NAMES = ["assemble", "spmv0", "cheb0", "cheb_coarse", "resid0", "multidot", "maxpy_norm", "maxpy",
-                  "delta_energy", "transfer", "coarse_solve", "resid_coarse", "pi_update", "cheb0_fused"]
+                  "delta_energy", "transfer", "coarse_solve", "resid_coarse", "pi_update", "cheb0_fused", "transport"]
 
     def profile(self, on: bool):
         self._check(self.L.seaice_profile_enable(self.h, 1 if on else 0))
@@ -390,6 +391,13 @@ class SeaIce:
         d = struct_dict(st)
         d["rc"] = rc
         return v_out, d
+
+    def transport(self, dt, v, A, h, A_in=1.0, h_in=0.0):
+        """(A, h) advanced by one explicit upwind step with velocity v (seaice_transport)."""
+        v, A, h = self.tensor(v, self.N), self.tensor(A, self.Nc), self.tensor(h, self.Nc)
+        Ao, ho = self.zeros(self.Nc), self.zeros(self.Nc)
+        self._check(self.L.seaice_transport(self.h, dt, _ptr(v), _ptr(A), _ptr(h), A_in, h_in, _ptr(Ao), _ptr(ho)))
+        return Ao, ho
 
     def solve_step_host(self, dt, t_new, h, A, v_prev, v_air, v_ocean, v_out):
         """Host (CPU, ideally pinned) torch tensors in and out: the end-to-end call."""

@@ -198,6 +198,44 @@ def problem1_inputs(n: int, L: float = L_DOMAIN, dt: float = 1800.0) -> StepInpu
                       v_ocean=np.zeros(2 * Nn), L=L)
 
 
+# ----------------------------------------------------------------------------- Problem II
+DAY = 86400.0
+
+
+def problem2_wind_nodal(n: int, t: float, L: float = L_DOMAIN) -> np.ndarray:
+    """PAPER.md Problem II atmosphere (Mehlmann 2021 benchmark) at time t [s]:
+    v_a = omega(x, y) v_max(t) R(alpha) (x - m(t)), R(alpha) = [[cos, sin], [-sin, cos]],
+    omega = exp(-|x - m| / 100 km) / 50, with x - m in km (reading G27: peak ~11 m/s);
+    v_max = 15 m/s * (-tanh((4 - t)(4 + t)/2)) for t in [0, 4] d, tanh((12 - t)(-4 + t)/2) for
+    t in [4, 8] d; alpha = 72 / 81 deg; m_x = m_y = 256 + 51.2 t km (t <= 4 d), 665.6 - 51.2 t km.
+    Interleaved nodal [2 (n+1)^2]."""
+    td = min(max(t / DAY, 0.0), 8.0)
+    if td <= 4.0:
+        vmax = -15.0 * math.tanh((4.0 - td) * (4.0 + td) / 2.0)
+        alpha = math.radians(72.0)
+        m = 256.0 + 51.2 * td
+    else:
+        vmax = 15.0 * math.tanh((12.0 - td) * (-4.0 + td) / 2.0)
+        alpha = math.radians(81.0)
+        m = 665.6 - 51.2 * td
+    X, Y = node_coords(n, L)
+    dxk, dyk = X / 1.0e3 - m, Y / 1.0e3 - m
+    om = np.exp(-np.sqrt(dxk ** 2 + dyk ** 2) / 100.0) / 50.0
+    ca, sa = math.cos(alpha), math.sin(alpha)
+    va = np.empty(2 * (n + 1) ** 2)
+    va[0::2] = om * vmax * (ca * dxk + sa * dyk)
+    va[1::2] = om * vmax * (-sa * dxk + ca * dyk)
+    return va
+
+
+def problem2_initial(n: int, L: float = L_DOMAIN):
+    """Problem II initial state: v = 0, A = 1, H = 0.3 m + 0.005 m (sin(60 x/1000 km)
+    + sin(30 y/1000 km)) at cell centres.  Returns (h, A, v)."""
+    X, Y = cell_centres(n, L)
+    h = 0.3 + 0.005 * (np.sin(60.0 * X / 1.0e6) + np.sin(30.0 * Y / 1.0e6))
+    return h, np.ones(n * n), np.zeros(2 * (n + 1) ** 2)
+
+
 def boundary_mask_nodes(n: int):
     i = np.arange(n + 1)
     I, J = np.meshgrid(i, i, indexing="xy")

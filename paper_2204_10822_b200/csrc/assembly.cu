@@ -437,8 +437,8 @@ void set_step_impl(Ctx& c, double dt, double t_new, const double* h, const doubl
 // triangle, 36 values) and the 8 element residual terms into shared memory (SoA, bank-conflict
 // free).  Phase 2: one thread per node gathers its residual pair and the 19 values of its
 // symmetric stencil row (stencil.cuh) from the four adjacent cells and writes them coalesced.
-// Each cell's quadrature-point algebra is done once per tile (1.16x recompute for the halo at
-// 31 x 8) instead of once per node (4x); every value is written once by one thread.
+// Each cell's quadrature-point algebra is done once per tile (1.13x recompute for the halo at
+// 15 x 16) instead of once per node (4x); every value is written once by one thread.
 //
 // Per-cell algebra: exact identities of the uniform Q1 cell (Walsh-Hadamard structure):
 //  * Phi = [phi_a] (rows phi_a = (1, xi_a, eta_a, xi_a eta_a)) is a signed Hadamard matrix, so a
@@ -820,16 +820,16 @@ __device__ __forceinline__ double gather_node_rows(int n, int Nn, int i0, int j0
   return r0 * r0 + r1 * r1;
 }
 
-// Persistent form: 2 CTAs per SM loop over the tiles (fixed assignment => fixed summation order
-// of the residual norm); while a tile is assembled, the next tile's inputs are prefetched into L2.
+// One CTA per tile (persistent CTAs with an L2 prefetch of the next tile measured no faster and
+// spilled registers).
 template <int TX, int TY>
 struct HadTile {
   static constexpr int TC = (TX + 1) * (TY + 1), NT = TC, SMEM = (kKE + 8) * TC * 8;
 };
 
 template <int KIND, int TX, int TY>
-__global__ void __launch_bounds__(HadTile<TX, TY>::NT, 2)
-    k_assemble_had(Phys ph, ElemH K, int Nn, int tiles_x, int ntiles, const double* __restrict__ v,
+__global__ void __launch_bounds__(HadTile<TX, TY>::NT, (HadTile<TX, TY>::NT <= 160 ? 4 : 2))
+    k_assemble_had(Phys ph, ElemH K, int Nn, int tiles_x, const double* __restrict__ v,
                    const double* __restrict__ pi, const double* __restrict__ P, const double* __restrict__ rhoh,
                    const double* __restrict__ vo, const double* __restrict__ F, double* __restrict__ Jst,
                    double* __restrict__ R, double* __restrict__ part) {
@@ -838,42 +838,18 @@ __global__ void __launch_bounds__(HadTile<TX, TY>::NT, 2)
   double* Ks = smem;             // [36][TC]
   double* Rs = smem + kKE * TC;  // [8][TC]
   __shared__ double sh[32];
-  const int n = ph.n, s = n + 1;
-  const long long Nc = (long long)n * n;
+  const int n = ph.n;
   const int t = threadIdx.x;
+  const int i0 = (blockIdx.x % tiles_x) * TX, j0 = (blockIdx.x / tiles_x) * TY;
+  {
+    const int ci = i0 - 1 + t % (TX + 1), cj = j0 - 1 + t / (TX + 1);
+    if (ci >= 0 && ci < n && cj >= 0 && cj < n) element_had<KIND, TC>(K, n, ci, cj, v, vo, pi, P, rhoh, Ks, Rs, t);
+  }
+  __syncthreads();
   double nrm = 0.0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int i0 = (tile % tiles_x) * TX, j0 = (tile / tiles_x) * TY;
-    {
-      const int ci = i0 - 1 + t % (TX + 1), cj = j0 - 1 + t / (TX + 1);
-      if (ci >= 0 && ci < n && cj >= 0 && cj < n) element_had<KIND, TC>(K, n, ci, cj, v, vo, pi, P, rhoh, Ks, Rs, t);
-    }
-    {
-      const int nt = tile + gridDim.x;
-      if (nt < ntiles) {
-        const int ci = (nt % tiles_x) * TX - 1 + t % (TX + 1), cj = (nt / tiles_x) * TY - 1 + t / (TX + 1);
-        if (ci >= 0 && ci < n && cj >= 0 && cj < n) {
-          const int cell = cj * n + ci, nd = cj * s + ci;
-          if (KIND == SEAICE_JAC_SV) {
-#pragma unroll
-            for (int r = 0; r < 12; ++r) asm volatile("prefetch.global.L2 [%0];" ::"l"(pi + r * Nc + cell));
-          }
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(P + cell));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(rhoh + cell));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(v + 2 * nd));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(v + 2 * (nd + s)));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(vo + 2 * nd));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(vo + 2 * (nd + s)));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(F + 2 * (nd + s + 1)));
-        }
-      }
-    }
-    __syncthreads();
-    if (t < TX * TY) {
-      const int i = i0 + t % TX, j = j0 + t / TX;
-      if (i <= n && j <= n) nrm += gather_node_rows<TX, TC>(n, Nn, i0, j0, i, j, Ks, Rs, F, Jst, R);
-    }
-    __syncthreads();  // Ks / Rs are rewritten by the next tile
+  if (t < TX * TY) {
+    const int i = i0 + t % TX, j = j0 + t / TX;
+    if (i <= n && j <= n) nrm = gather_node_rows<TX, TC>(n, Nn, i0, j0, i, j, Ks, Rs, F, Jst, R);
   }
   const double bs = block_sum(nrm, sh);
   if (threadIdx.x == 0) part[blockIdx.x] = bs;
@@ -882,23 +858,17 @@ __global__ void __launch_bounds__(HadTile<TX, TY>::NT, 2)
 template <int KIND, int TX, int TY>
 static int launch_assemble_had_t(Ctx& c, const double* v, const double* pi, double* R) {
   using HT = HadTile<TX, TY>;
-  static int ctas = 0;
-  if (!ctas) {
+  static bool attr = false;
+  if (!attr) {
     SI_CUDA(cudaFuncSetAttribute(k_assemble_had<KIND, TX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, HT::SMEM));
-    int per_sm = 0, dev = 0, sms = 0;
-    SI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_assemble_had<KIND, TX, TY>, HT::NT, HT::SMEM));
-    SI_CUDA(cudaGetDevice(&dev));
-    SI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    ctas = (per_sm > 0 ? per_sm : 1) * sms;
+    attr = true;
   }
   upload_qc();
   const int tx = (c.n + 1 + TX - 1) / TX, ty = (c.n + 1 + TY - 1) / TY;
-  const int ntiles = tx * ty;
-  static const bool persist = getenv("SEAICE_ASM_PERSIST") && atoi(getenv("SEAICE_ASM_PERSIST"));  // tuning aid
-  const int g = (persist && ctas < ntiles) ? ctas : ntiles;
+  const int g = tx * ty;
   c.part.ensure(c.al, g + 64);
   prof_begin(c);
-  k_assemble_had<KIND, TX, TY><<<g, HT::NT, HT::SMEM, c.s>>>(c.ph, make_elemh(c.ph), c.Nn, tx, ntiles, v, pi, c.P.get(),
+  k_assemble_had<KIND, TX, TY><<<g, HT::NT, HT::SMEM, c.s>>>(c.ph, make_elemh(c.ph), c.Nn, tx, v, pi, c.P.get(),
                                                              c.rhoh.get(), c.vocean.get(), c.F.get(), c.Jst.get(), R,
                                                              c.part.get());
   SI_LAUNCHED(c);
@@ -908,9 +878,13 @@ static int launch_assemble_had_t(Ctx& c, const double* v, const double* pi, doub
 
 template <int KIND>
 static int launch_assemble_had(Ctx& c, const double* v, const double* pi, double* R) {
-  static const int variant = getenv("SEAICE_ASM_TILE") ? atoi(getenv("SEAICE_ASM_TILE")) : 0;  // tuning aid
-  if (variant == 1) return launch_assemble_had_t<KIND, 15, 16>(c, v, pi, R);
-  return launch_assemble_had_t<KIND, 31, 8>(c, v, pi, R);
+  // 15 x 16 node tiles (16 x 17 cells: 1.13x element recompute, 2 CTAs/SM) measured fastest on B200
+  // (config 5: 2.18 ms vs 2.23 ms for 31 x 8, 2.27 ms for 31 x 4, 2.47 ms for 15 x 8 at 4 CTAs/SM)
+  static const int variant = getenv("SEAICE_ASM_TILE") ? atoi(getenv("SEAICE_ASM_TILE")) : 1;  // tuning aid
+  if (variant == 0) return launch_assemble_had_t<KIND, 31, 8>(c, v, pi, R);
+  if (variant == 2) return launch_assemble_had_t<KIND, 15, 8>(c, v, pi, R);
+  if (variant == 3) return launch_assemble_had_t<KIND, 31, 4>(c, v, pi, R);
+  return launch_assemble_had_t<KIND, 15, 16>(c, v, pi, R);
 }
 
 static void launch_residual(Ctx& c, const double* v, double* R) {

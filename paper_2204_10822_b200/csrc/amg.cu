@@ -1206,6 +1206,43 @@ __global__ void __launch_bounds__(FusedGeom<M>::NT, (FusedGeom<M>::NT <= 256 ? 2
   const int node = gj * s + gi;
   const bool interior = gi > 0 && gi < n && gj > 0 && gj < n;
   const int sidx = (lj + 1) * Gm::HX + (li + 1);
+  // Halo values of d_0 (outermost ring for pre-smoothing, the whole d region for post-smoothing)
+  // are requested first, so that their loads overlap the stencil-row loads below instead of
+  // following them (at most 2 entries per thread).
+  constexpr int NRING = 2 * Gm::HX + 2 * (Gm::HY - 2), NREG = Gm::HX * Gm::HY;
+  constexpr int NH = ((NRING > NREG ? NRING : NREG) + Gm::NT - 1) / Gm::NT;
+  double2 hb[NH];
+  double4 hd[NH];
+  int hidx[NH];
+#pragma unroll
+  for (int q = 0; q < NH; ++q) {
+    const int idx = t + q * Gm::NT;
+    hidx[q] = -1;
+    hb[q] = make_double2(0.0, 0.0);
+    hd[q] = make_double4(0.0, 0.0, 0.0, 0.0);
+    int hx = 0, hy = 0;
+    if (pre) {
+      if (idx >= NRING) continue;
+      if (idx < Gm::HX) { hx = idx; hy = 0; }
+      else if (idx < 2 * Gm::HX) { hx = idx - Gm::HX; hy = Gm::HY - 1; }
+      else { const int qq = idx - 2 * Gm::HX; hx = (qq & 1) ? Gm::HX - 1 : 0; hy = 1 + (qq >> 1); }
+    } else {
+      if (idx >= NREG) continue;
+      hx = idx % Gm::HX;
+      hy = idx / Gm::HX;
+    }
+    hidx[q] = hy * Gm::HX + hx;
+    const int hi = i0 - M + hx, hj = j0 - M + hy;
+    if (hi >= 0 && hi <= n && hj >= 0 && hj <= n) {
+      const int nd = hj * s + hi;
+      if (pre) {
+        hb[q] = rin[nd];
+        hd[q] = reinterpret_cast<const double4*>(dinv)[nd];
+      } else {
+        hb[q] = d0g[nd];
+      }
+    }
+  }
   // this node's stencil row (read once for the M steps), r_0, Dinv, x_0
   double Jr[36];
   double2 rv = make_double2(0.0, 0.0), xa = make_double2(0.0, 0.0);
@@ -1229,26 +1266,15 @@ __global__ void __launch_bounds__(FusedGeom<M>::NT, (FusedGeom<M>::NT <= 256 ? 2
   if (pre) {  // d_0 = ith Dinv b on the tile + M rings
     sd[0][sidx] = inside ? make_double2(k.ith * (D.x * rv.x + D.y * rv.y), k.ith * (D.z * rv.x + D.w * rv.y))
                          : make_double2(0.0, 0.0);
-    for (int idx = t; idx < 2 * Gm::HX + 2 * (Gm::HY - 2); idx += Gm::NT) {  // outermost ring
-      int hx, hy;
-      if (idx < Gm::HX) { hx = idx; hy = 0; }
-      else if (idx < 2 * Gm::HX) { hx = idx - Gm::HX; hy = Gm::HY - 1; }
-      else { const int q = idx - 2 * Gm::HX; hx = (q & 1) ? Gm::HX - 1 : 0; hy = 1 + (q >> 1); }
-      const int hi = i0 - M + hx, hj = j0 - M + hy;
-      double2 dv = make_double2(0.0, 0.0);
-      if (hi >= 0 && hi <= n && hj >= 0 && hj <= n) {
-        const int nd = hj * s + hi;
-        const double2 b0 = rin[nd];
-        const double4 Dr = reinterpret_cast<const double4*>(dinv)[nd];
-        dv = make_double2(k.ith * (Dr.x * b0.x + Dr.y * b0.y), k.ith * (Dr.z * b0.x + Dr.w * b0.y));
-      }
-      sd[0][hy * Gm::HX + hx] = dv;
-    }
+#pragma unroll
+    for (int q = 0; q < NH; ++q)
+      if (hidx[q] >= 0)
+        sd[0][hidx[q]] = make_double2(k.ith * (hd[q].x * hb[q].x + hd[q].y * hb[q].y),
+                                      k.ith * (hd[q].z * hb[q].x + hd[q].w * hb[q].y));
   } else {  // stage d_0 on the tile + M rings (zero outside the domain)
-    for (int idx = t; idx < Gm::HX * Gm::HY; idx += Gm::NT) {
-      const int hi = i0 - M + idx % Gm::HX, hj = j0 - M + idx / Gm::HX;
-      sd[0][idx] = (hi >= 0 && hi <= n && hj >= 0 && hj <= n) ? d0g[hj * s + hi] : make_double2(0.0, 0.0);
-    }
+#pragma unroll
+    for (int q = 0; q < NH; ++q)
+      if (hidx[q] >= 0) sd[0][hidx[q]] = hb[q];
   }
   __syncthreads();
   // steps 1 .. M-1

@@ -85,6 +85,9 @@ typedef struct {
   int32_t cheb_fused;      /* 1 (default): finest-level Chebyshev(3) as one temporally blocked launch
                               (same arithmetic per node and step); 0: one launch per step */
   int32_t cheb_degree0;    /* Chebyshev degree on the finest level (0: cheb_degree) */
+  int32_t matfree;         /* 0 (default): FGMRES applies the assembled stencil J; 1: FGMRES applies
+                              J(v, pi) matrix-free from the (v, pi) of the
+                              last assembly, the AMG hierarchy still built from the assembled J */
 } seaice_params;
 
 /* Compressed-sparse-row view (scalar rows). Index arrays int32, values fp64. */
@@ -173,6 +176,14 @@ int seaice_spmv(seaice_ctx* ctx, const double* x, double* y);
  * no synchronisation.  EINVAL on NULL / aliased buffers or dt < 0 / non-finite. */
 int seaice_transport(seaice_ctx* ctx, double dt, const double* v, const double* A, const double* H,
                      double A_in, double H_in, double* A_out, double* H_out);
+
+/* Matrix-free Jacobian apply y = J(v, pi) x (eq:linearSVNewton P:512-525 with
+ * eq:modification P:534-539; the JFNK discussion P:545-653): the element matrices of the ctx's
+ * jacobian kind are recomputed per cell (same arithmetic as seaice_assemble_jacobian) and applied
+ * to x without storing J; Dirichlet rows return x, Dirichlet columns are eliminated.  v, x, y:
+ * [2(n+1)^2] interleaved (device); pi: [3][4][n*n] (device) or NULL = ctx pi.  Needs set_step.
+ * Enqueued on the ctx stream.  EINVAL on NULL v / x / y or y aliasing x. */
+int seaice_jv_matfree(seaice_ctx* ctx, const double* v, const double* pi, const double* x, double* y);
 
 /* Build the AMG hierarchy of the last assembled Jacobian on the GPU: node-block
  * strength, MIS(2) aggregation, rigid-body tentative prolongator, smoothed

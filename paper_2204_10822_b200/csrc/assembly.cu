@@ -568,7 +568,7 @@ __device__ __forceinline__ void cp_async8(unsigned saddr, const double* g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(g) : "memory");
 }
 
-template <int KIND, int TC>
+template <int KIND, int TC, bool RES = true>
 __device__ __forceinline__ void element_had(const ElemH& K, int n, int ci, int cj, const double* __restrict__ v,
                                             const double* __restrict__ vo, const double* __restrict__ pi,
                                             const double* __restrict__ P, const double* __restrict__ rhoh,
@@ -678,6 +678,7 @@ __device__ __forceinline__ void element_had(const ElemH& K, int n, int ci, int c
     slot[7 * TC] = K.kd * fma(wyr, wy, nw);
     slot[8 * TC] = K.kd * (wxr * wy);
     // element residual -A(v, phi_{a,k}) (eq:A) = sum_a N_a MX + dN_a/dx CX + dN_a/dy CZ (x row)
+    if (!RES) continue;
     const double wdcn = K.wdtco * nw;
     const double MX = fma(wdcn, wx, wrh * vx), MY = fma(wdcn, wy, wrh * vy);
     const double m = mP * rD;  // -w dt P/(Delta dx)
@@ -689,8 +690,10 @@ __device__ __forceinline__ void element_had(const ElemH& K, int n, int ci, int c
       Ra[2 * a + 1] = fma(Na, MY, fma(gy, CY, fma(gx, CZ, Ra[2 * a + 1])));
     }
   }
+  if (RES) {
 #pragma unroll
-  for (int p = 0; p < 8; ++p) Rs[p * TC + t] = Ra[p];
+    for (int p = 0; p < 8; ++p) Rs[p * TC + t] = Ra[p];
+  }
   // q-moments of the parked values: mom[0] = sum, [1] = sum xi_q/g, [2] = sum eta_q/g, [3] = sum xi_q eta_q * 3
   auto moments = [&](int j, double mom[4]) {
     const double* sl = Ks + j * TC + t;
@@ -876,6 +879,105 @@ static int launch_assemble_had_t(Ctx& c, const double* v, const double* pi, doub
   return g;
 }
 
+// ------------------------------------------------------------------ NEXT-4: matrix-free J x
+// Phase 2 of the matrix-free apply: (J x)_node from the element matrices of its four cells and x
+// at its 3 x 3 node neighbourhood; Dirichlet columns are eliminated (x_b taken as 0) and Dirichlet
+// rows return x, exactly as in the assembled stencil.
+template <int TX, int TC>
+__device__ __forceinline__ void gather_node_apply(int n, int i0, int j0, int i, int j, const double* __restrict__ Ks,
+                                                  const double2* __restrict__ x, double2* __restrict__ y) {
+  const int s = n + 1;
+  const int node = j * s + i;
+  if (!(i > 0 && i < n && j > 0 && j < n)) {
+    y[node] = x[node];
+    return;
+  }
+  double2 xn[9];
+#pragma unroll
+  for (int sl = 0; sl < 9; ++sl) {
+    const int ii = i + sl % 3 - 1, jj = j + sl / 3 - 1;
+    const bool bnd = (ii == 0 || ii == n || jj == 0 || jj == n);
+    xn[sl] = bnd ? make_double2(0.0, 0.0) : __ldg(x + jj * s + ii);
+  }
+  const int lc0 = (i - i0) + (j - j0) * (TX + 1);
+  double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc) {
+    const int ax = 1 - (cc & 1), ay = 1 - (cc >> 1);
+    const int lc = lc0 + (cc & 1) + (cc >> 1) * (TX + 1);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int bx = ox(b), by = oy(b);
+      const double2 xv = xn[(by - ay + 1) * 3 + (bx - ax + 1)];
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const int p = 2 * lidx(ax, ay) + k, q = 2 * b + m;
+          const double e = Ks[(p <= q ? ke_idx(p, q) : ke_idx(q, p)) * TC + lc];
+          const double xm = m ? xv.y : xv.x;
+          if (k == 0) y0 = fma(e, xm, y0);
+          else y1 = fma(e, xm, y1);
+        }
+    }
+  }
+  y[node] = make_double2(y0, y1);
+}
+
+template <int KIND, int TX, int TY>
+__global__ void __launch_bounds__(HadTile<TX, TY>::NT, (HadTile<TX, TY>::NT <= 160 ? 4 : 2))
+    k_jv_matfree(Phys ph, ElemH K, int tiles_x, const double* __restrict__ v, const double* __restrict__ pi,
+                 const double* __restrict__ P, const double* __restrict__ rhoh, const double* __restrict__ vo,
+                 const double2* __restrict__ x, double2* __restrict__ y) {
+  constexpr int TC = HadTile<TX, TY>::TC;
+  extern __shared__ double smem[];
+  double* Ks = smem;             // [36][TC]
+  double* Rs = smem + kKE * TC;  // [8][TC] (input staging only)
+  const int n = ph.n;
+  const int t = threadIdx.x;
+  const int i0 = (blockIdx.x % tiles_x) * TX, j0 = (blockIdx.x / tiles_x) * TY;
+  {
+    const int ci = i0 - 1 + t % (TX + 1), cj = j0 - 1 + t / (TX + 1);
+    if (ci >= 0 && ci < n && cj >= 0 && cj < n)
+      element_had<KIND, TC, false>(K, n, ci, cj, v, vo, pi, P, rhoh, Ks, Rs, t);
+  }
+  __syncthreads();
+  if (t < TX * TY) {
+    const int i = i0 + t % TX, j = j0 + t / TX;
+    if (i <= n && j <= n) gather_node_apply<TX, TC>(n, i0, j0, i, j, Ks, x, y);
+  }
+}
+
+template <int KIND>
+static void launch_jv_matfree(Ctx& c, const double* v, const double* pi, const double* x, double* y) {
+  constexpr int TX = 15, TY = 16;
+  using HT = HadTile<TX, TY>;
+  static bool attr = false;
+  if (!attr) {
+    SI_CUDA(cudaFuncSetAttribute(k_jv_matfree<KIND, TX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, HT::SMEM));
+    attr = true;
+  }
+  upload_qc();
+  const int tx = (c.n + 1 + TX - 1) / TX, ty = (c.n + 1 + TY - 1) / TY;
+  prof_begin(c);
+  k_jv_matfree<KIND, TX, TY><<<tx * ty, HT::NT, HT::SMEM, c.s>>>(c.ph, make_elemh(c.ph), tx, v, pi, c.P.get(), c.rhoh.get(),
+                                                                 c.vocean.get(), reinterpret_cast<const double2*>(x),
+                                                                 reinterpret_cast<double2*>(y));
+  SI_LAUNCHED(c);
+  // algorithmic bytes: v, v_o, x read, y written per node; pi, P, rho_i h per cell
+  prof_end(c, PC_MATFREE, 64.0 * c.Nn + 112.0 * c.Nc);
+}
+
+void jv_matfree_impl(Ctx& c, const double* v, const double* pi, const double* x, double* y) {
+  SI_CHECK(c.step_set, SEAICE_ESTATE, "jv_matfree before set_step");
+  SI_CHECK(v && x && y, SEAICE_EINVAL, "jv_matfree: NULL vector");
+  SI_CHECK(x != y, SEAICE_EINVAL, "jv_matfree: y must not alias x");
+  const double* pp = pi ? pi : c.pi.get();
+  if (c.p.jacobian == SEAICE_JAC_SV) launch_jv_matfree<SEAICE_JAC_SV>(c, v, pp, x, y);
+  else if (c.p.jacobian == SEAICE_JAC_STD) launch_jv_matfree<SEAICE_JAC_STD>(c, v, pp, x, y);
+  else launch_jv_matfree<SEAICE_JAC_PICARD>(c, v, pp, x, y);
+}
+
 template <int KIND>
 static int launch_assemble_had(Ctx& c, const double* v, const double* pi, double* R) {
   // 15 x 16 node tiles (16 x 17 cells: 1.13x element recompute, 2 CTAs/SM) measured fastest on B200
@@ -921,6 +1023,12 @@ void assemble_impl(Ctx& c, const double* v, const double* pi, bool jac, double* 
   if (jac) {
     c.assembled = true;
     c.amg_ready = false;
+    if (c.p.matfree) {  // the matrix-free FGMRES operator needs the linearisation point
+      c.mf_v.ensure(c.al, c.N);
+      c.mf_pi.ensure(c.al, 12LL * c.Nc);
+      SI_CUDA(cudaMemcpyAsync(c.mf_v.get(), v, sizeof(double) * c.N, cudaMemcpyDeviceToDevice, c.s));
+      SI_CUDA(cudaMemcpyAsync(c.mf_pi.get(), pp, sizeof(double) * 12 * c.Nc, cudaMemcpyDeviceToDevice, c.s));
+    }
   }
 }
 

@@ -98,6 +98,7 @@ enum ProfClass {
   PC_PIUPD = 12,    // K12 dual update
   PC_CHEB0F = 13,   // K4 three Chebyshev steps fused (temporal blocking), finest level
   PC_TRANSPORT = 14,  // NEXT-3 explicit upwind transport of A, h
+  PC_MATFREE = 15,  // NEXT-4 matrix-free Jacobian apply
   PC_NCLASS = 16
 };
 struct Prof {
@@ -136,6 +137,7 @@ struct Ctx {
   // finest-level Jacobian: upper half of the symmetric 3x3 node stencil of 2x2 blocks,
   // 19 values per node, slot-major SoA (layout in stencil.cuh)
   DBuf<double> Jst;
+  DBuf<double> mf_v, mf_pi;  // (v, pi) of the last assembly, for the matrix-free FGMRES operator
   DBuf<double> R;  // residual of the last assemble
   double last_res_norm = 0.0;
   // scalar CSR view (built on demand)
@@ -241,6 +243,7 @@ inline void prof_end(Ctx& c, int k, double bytes = 0.0) {
 void set_step_impl(Ctx& c, double dt, double t_new, const double* h, const double* A, const double* v_prev,
                    const double* v_air, const double* v_ocean, const double* load);
 void assemble_impl(Ctx& c, const double* v, const double* pi, bool jacobian, double* r_out, double* norm_host);
+void jv_matfree_impl(Ctx& c, const double* v, const double* pi, const double* x, double* y);
 void transport_impl(Ctx& c, double dt, const double* v, const double* A, const double* H, double A_in, double H_in,
                     double* Ao, double* Ho);
 void build_csr_view(Ctx& c, seaice_csr* out);

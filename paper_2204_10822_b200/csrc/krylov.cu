@@ -10,7 +10,12 @@
 
 namespace seaice {
 
-static void apply_A(Ctx& c, const double* x, double* y) { stencil_spmv(c, x, y); }
+// FGMRES operator: the assembled stencil J, or (matfree = 1) J(v, pi) applied
+// matrix-free at the linearisation point saved by the last assembly
+static void apply_A(Ctx& c, const double* x, double* y) {
+  if (c.p.matfree) jv_matfree_impl(c, c.mf_v.get(), c.mf_pi.get(), x, y);
+  else stencil_spmv(c, x, y);
+}
 
 __global__ void k_point_jacobi(int Nn, const double* __restrict__ J, const double* __restrict__ r,
                                double* __restrict__ z) {

@@ -35,7 +35,7 @@ class Params(C.Structure):
                 ("cheb_lower", C.c_double), ("cheb_upper", C.c_double), ("power_iters", C.c_int32),
                 ("project_pi", C.c_int32), ("amg_seed", C.c_uint64), ("agg_dist0", C.c_int32),
                 ("agg_dist", C.c_int32), ("cheb_fused", C.c_int32),
-                ("cheb_degree0", C.c_int32)]
+                ("cheb_degree0", C.c_int32), ("matfree", C.c_int32)]
 
 
 ALLOC_T = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -124,6 +124,7 @@ def lib(build_if_missing: bool = True):
             "seaice_assemble_jacobian": (C.c_int, [VP, VP, VP, P(CSR)]),
             "seaice_spmv": (C.c_int, [VP, VP, VP]),
             "seaice_transport": (C.c_int, [VP, D, VP, VP, VP, D, D, VP, VP]),
+            "seaice_jv_matfree": (C.c_int, [VP, VP, VP, VP, VP]),
             "seaice_amg_setup": (C.c_int, [VP, P(I32), P(D)]),
             "seaice_amg_level": (C.c_int, [VP, I32, P(BSR), P(BSR), VP]),
             "seaice_precond_apply": (C.c_int, [VP, VP, VP]),
@@ -260,7 +261,7 @@ class SeaIce:
         return int(self.L.seaice_launch_count(self.h))
 
     PROF_NAMES = ["assemble", "spmv0", "cheb0", "cheb_coarse", "resid0", "multidot", "maxpy_norm", "maxpy",
-                  "delta_energy", "transfer", "coarse_solve", "resid_coarse", "pi_update", "cheb0_fused", "transport"]
+                  "delta_energy", "transfer", "coarse_solve", "resid_coarse", "pi_update", "cheb0_fused", "transport", "jv_matfree"]
 
     def profile(self, on: bool):
         self._check(self.L.seaice_profile_enable(self.h, 1 if on else 0))
@@ -391,6 +392,14 @@ class SeaIce:
         d = struct_dict(st)
         d["rc"] = rc
         return v_out, d
+
+    def jv_matfree(self, v, x, pi=None):
+        """y = J(v, pi) x without storing J (seaice_jv_matfree)."""
+        v, x = self.tensor(v, self.N), self.tensor(x, self.N)
+        pi = None if pi is None else self.tensor(pi, 12 * self.Nc)
+        y = self.zeros(self.N)
+        self._check(self.L.seaice_jv_matfree(self.h, _ptr(v), _ptr(pi), _ptr(x), _ptr(y)))
+        return y
 
     def transport(self, dt, v, A, h, A_in=1.0, h_in=0.0):
         """(A, h) advanced by one explicit upwind step with velocity v (seaice_transport)."""

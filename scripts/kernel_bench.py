@@ -60,6 +60,13 @@ y = torch.empty_like(x)
 ms = timed(lambda: ctx.spmv(x))
 b = 184.0 * Nn  # symmetric stencil (152 B) + x, y per node
 out["spmv"] = {"ms": ms, "alg_bytes": b, "gbs": b / ms / 1e6, "frac": b / ms / 1e6 / peak}
+# NEXT-4: matrix-free apply of the same operator (element algebra recomputed per call)
+yb = torch.empty_like(x)
+ms = timed(lambda: ctx.jv_matfree(v, x))
+b = 64.0 * Nn + 112.0 * Nc
+out["jv_matfree"] = {"ms": ms, "alg_bytes": b, "gbs": b / ms / 1e6, "frac": b / ms / 1e6 / peak,
+                     "vs_spmv": ms / out["spmv"]["ms"],
+                     "note": "fp64-bound: per-cell element algebra recomputed each apply (ms incl. the binding's output allocation)"}
 nl, oc = ctx.amg_setup()
 out["amg"] = {"levels": nl, "op_complexity": oc, "setup_ms": timed(lambda: ctx.amg_setup(), reps=3)}
 ms = timed(lambda: ctx.precond_apply(x))

@@ -299,6 +299,8 @@ int seaice_destroy(seaice_ctx* h) {
   if (c.cap_stream) cudaStreamDestroy(c.cap_stream);
   if (c.ev0) cudaEventDestroy(c.ev0);
   if (c.ev1) cudaEventDestroy(c.ev1);
+  for (auto e : c.arn_ev)
+    if (e) cudaEventDestroy(e);
   cudaStreamSynchronize(c.s);
   delete h;
   return SEAICE_OK;

@@ -180,6 +180,7 @@ struct Ctx {
   DBuf<double> st_h, st_A, st_vp, st_va, st_vo, st_v;
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t arn_ev[2] = {nullptr, nullptr};  // FGMRES: scalars of Arnoldi step j landed in hbuf slot j & 1
 };
 
 inline void count_launch(Ctx& c, int k = 1) { c.launches += k; }
@@ -265,6 +266,9 @@ void copy(Ctx& c, double* dst, const double* src, long long n);
 // FGMRES helpers: h[0..j] = V[0..j]^T w ; w -= V h, return ||w||
 // h = V[:, :k]^T w, w -= V h, vnext = w / ||w||; returns ||w|| (one host sync)
 double arnoldi_step(Ctx& c, const double* V, long long ld, int k, double* w, long long n, double* vnext, double* h_host);
+// device part of one Arnoldi step; h (k values) and ||w||^2 are copied to hbuf[64 slot .. ] and
+// hbuf[64 slot + 63] without synchronising
+void arnoldi_enqueue(Ctx& c, const double* V, long long ld, int k, double* w, long long n, double* vnext, int slot);
 void multi_axpy(Ctx& c, const double* Z, long long ld, int k, const double* y_host, double* x, long long n);
 
 // krylov.cu

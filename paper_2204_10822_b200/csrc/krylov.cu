@@ -52,6 +52,8 @@ int fgmres_impl(Ctx& c, const double* b, double* x, seaice_krylov_stats* st) {
   double* V = c.V.get();
   double* Z = c.Z.get();
   double* w = c.w.get();
+  for (auto& e : c.arn_ev)
+    if (!e) SI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   fill(c, x, 0.0, N);
   const double bnorm = norm2(c, b, N);
   seaice_krylov_stats S{0, 0, 1, 0.0, 0.0};
@@ -73,12 +75,25 @@ int fgmres_impl(Ctx& c, const double* b, double* x, seaice_krylov_stats* st) {
     g[0] = beta;
     scal_copy(c, 1.0 / beta, r, V, N);
     int jd = 0;
-    for (int j = 0; j < m; ++j) {
+    // Arnoldi steps are enqueued one ahead: step j + 1 (V-cycle, SpMV, orthogonalisation; all on
+    // the device, v_{j+1} normalised there) is queued before the host waits for step j's scalars,
+    // so the GPU does not idle during the host's Givens update.  A step queued past convergence
+    // is discarded (it only writes Z_{j+1}, w, V_{j+2} and its own scalar slot).
+    auto enqueue = [&](int j) {
       double* vj = V + (long long)j * N;
       double* zj = Z + (long long)j * N;
       precond_apply(c, vj, zj);
       apply_A(c, zj, w);
-      const double hn = arnoldi_step(c, V, N, j + 1, w, N, V + (long long)(j + 1) * N, h.data());
+      arnoldi_enqueue(c, V, N, j + 1, w, N, V + (long long)(j + 1) * N, j & 1);
+      SI_CUDA(cudaEventRecord(c.arn_ev[j & 1], c.s));
+    };
+    enqueue(0);
+    for (int j = 0; j < m; ++j) {
+      if (j + 1 < m && its + 1 < c.p.krylov_maxit) enqueue(j + 1);
+      SI_CUDA(cudaEventSynchronize(c.arn_ev[j & 1]));
+      const double* hh = c.hbuf + 64 * (j & 1);
+      for (int i = 0; i <= j; ++i) h[i] = hh[i];
+      const double hn = std::sqrt(hh[63]);
       SI_CHECK(std::isfinite(hn), SEAICE_ENONFINITE, "fgmres: non-finite Arnoldi vector");
       for (int i = 0; i <= j; ++i) H[i * m + j] = h[i];
       H[(j + 1) * m + j] = hn;

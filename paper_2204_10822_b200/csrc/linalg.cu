@@ -239,17 +239,16 @@ __global__ void k_normalize(long long n, const double* __restrict__ w, const dou
     out[i] = a * w[i];
 }
 
-double arnoldi_step(Ctx& c, const double* V, long long ld, int k, double* w, long long n, double* vnext,
-                    double* h_host) {
+void arnoldi_enqueue(Ctx& c, const double* V, long long ld, int k, double* w, long long n, double* vnext, int slot) {
   SI_CHECK(n % 2 == 0 && ld % 2 == 0, SEAICE_EINVAL, "arnoldi: odd length");
-  SI_CHECK(k <= 64, SEAICE_EINVAL, "arnoldi: k > 64");
+  SI_CHECK(k <= 63, SEAICE_EINVAL, "arnoldi: k > 63");
   const int g = red_grid(n / 2);
   c.part.ensure(c.al, (size_t)g * (k + 8));
-  double* hd = c.scal.get() + 64;   // h (k values)
-  double* n2d = c.scal.get() + 200;  // ||w||^2
+  double* hd = c.scal.get() + 64 + 96 * slot;  // h (k values), then ||w||^2 at +64
+  double* n2d = hd + 64;
   const double2* V2 = reinterpret_cast<const double2*>(V);
-  prof_begin(c);
   const double2* w2 = reinterpret_cast<const double2*>(w);
+  prof_begin(c);
   k_multidot<<<dim3(g, (k + kMDC - 1) / kMDC), kMDT, 0, c.s>>>(n / 2, V2, ld / 2, k, w2, c.part.get());
   SI_LAUNCHED(c);
   prof_end(c, PC_MDOT, 8.0 * (k + 1) * n);
@@ -262,11 +261,19 @@ double arnoldi_step(Ctx& c, const double* V, long long ld, int k, double* w, lon
   k_sum_cols<<<1, 1024, 0, c.s>>>(c.part.get(), g, 1, n2d);
   k_normalize<<<vgrid(n), kThreads, 0, c.s>>>(n, w, n2d, vnext);
   SI_LAUNCHED(c);
-  SI_CUDA(cudaMemcpyAsync(c.hbuf, hd, sizeof(double) * k, cudaMemcpyDeviceToHost, c.s));
-  SI_CUDA(cudaMemcpyAsync(c.hbuf + 128, n2d, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+  double* hh = c.hbuf + 64 * slot;
+  SI_CUDA(cudaMemcpyAsync(hh, hd, sizeof(double) * k, cudaMemcpyDeviceToHost, c.s));
+  SI_CUDA(cudaMemcpyAsync(hh + 63, n2d, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+}
+
+// One Arnoldi orthogonalisation step with a single host synchronisation (kept for callers that
+// do not pipeline): h = V^T w, w -= V h, vnext = w / ||w||; returns ||w||.
+double arnoldi_step(Ctx& c, const double* V, long long ld, int k, double* w, long long n, double* vnext,
+                    double* h_host) {
+  arnoldi_enqueue(c, V, ld, k, w, n, vnext, 0);
   SI_CUDA(cudaStreamSynchronize(c.s));
   std::memcpy(h_host, c.hbuf, sizeof(double) * k);
-  return std::sqrt(c.hbuf[128]);
+  return std::sqrt(c.hbuf[63]);
 }
 
 // x += sum_i y_i Z_i

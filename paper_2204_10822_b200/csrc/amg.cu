@@ -1814,7 +1814,9 @@ void vgraph_destroy(Ctx& c);
 
 void amg_setup_impl(Ctx& c) {
   SI_CHECK(c.assembled, SEAICE_ESTATE, "amg_setup before assemble");
+  tick(c, nullptr, 0);
   vgraph_destroy(c);
+  tick(c, "graph_free", 0);
   // the level pool keeps every buffer (grow-only) across setups; level 0's pattern is fixed
   if (c.lv.empty()) {
     c.lv.emplace_back();
@@ -1830,6 +1832,7 @@ void amg_setup_impl(Ctx& c) {
   L0.B.ensure(c.al, (size_t)c.Nn * 6);
   k_level0_nullspace<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.p.L, L0.B.get());
   SI_LAUNCHED(c);
+  tick(c, "to_bsr", 0);
   long long nnz_total = 0;
   const long long nnz0 = L0.nnzb * 4;
   for (int lvl = 0;; ++lvl) {
@@ -1862,8 +1865,10 @@ void amg_setup_impl(Ctx& c) {
     ++c.nlev;
     if (Lf.b == 2) build_transfer<2>(c, Lf, Lc, lvl, na, S);
     else build_transfer<3>(c, Lf, Lc, lvl, na, S);
+    tick(c, nullptr, lvl);
     tile_copy(c, Lf.PvalT, Lf.Pval.get(), Lf.Pnnzb, Lf.b * 3);
     tile_copy(c, Lf.RvalT, Lf.Rval.get(), Lf.Rnnzb, 3 * Lf.b);
+    tick(c, "tile_PR", lvl);
   }
   Level& Lc = c.lv[c.nlev - 1];
   const long long nd = (long long)Lc.nb * Lc.b;
@@ -1876,6 +1881,7 @@ void amg_setup_impl(Ctx& c) {
   SI_CHECK(!(flag & 8), SEAICE_ENONFINITE, "AMG: coarse matrix not positive definite");
   c.op_complexity = (double)nnz_total / (double)nnz0;
   c.amg_ready = true;
+  tick(c, "finish", c.nlev - 1);
 }
 
 // ------------------------------------------------------------------ host: V-cycle

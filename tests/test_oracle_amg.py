@@ -1,0 +1,121 @@
+"""CPU pins of oracle/amg.py (the AMG definition shared with the GPU path) by
+properties the algebra fixes, independent of the oracle's own formulas: MIS(2) independence at
+distance 2 and maximality; one aggregate per non-isolated node; orthonormal tentative columns that
+reproduce the near-nullspace; SPD Galerkin operators whose energy equals the fine energy of the
+prolongated vector; the Chebyshev error polynomial in closed form; a symmetric V-cycle; and an
+exact solve when the hierarchy has a single level (checked against an LU solve)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from oracle import amg
+from oracle import model as M
+from paper_2204_10822_b200 import workloads as wl
+
+PRM = wl.PhysParams()
+
+
+def _jacobian(n, seed=5, amp=0.05):
+    _, inp = wl.custom_inputs(n, seed=seed)
+    pb = M.Problem(inp, PRM)
+    v = wl.random_velocity(n, seed + 1, amp=amp)
+    pi = wl.random_pi(n, seed + 2)
+    return pb, pb.jacobian(v, pi, "sv").tocsr()
+
+
+@pytest.fixture(scope="module")
+def hier():
+    pb, J = _jacobian(24)
+    return pb, J, amg.setup(J, pb, coarse_max_dof=60)
+
+
+def test_mis2_is_distance2_independent_and_maximal():
+    pb, J = _jacobian(20)
+    G = amg.strength(J, 2, 0.04)
+    roots, isolated, _ = amg.mis2(G, 0, 0)
+    C = (G + sp.identity(G.shape[0], format="csr")).tocsr()
+    C2 = (C @ C).tocsr()  # distance <= 2 reachability
+    R = np.where(roots)[0]
+    sub = C2[R][:, R].tocoo()
+    assert np.all(sub.row == sub.col), "two roots within distance 2"
+    covered = np.asarray(C2[:, R].sum(axis=1)).ravel() > 0
+    assert np.all(covered | isolated), "a non-isolated node is farther than 2 from every root"
+
+
+def test_aggregates_partition_non_isolated_nodes():
+    pb, J = _jacobian(20)
+    G = amg.strength(J, 2, 0.04)
+    roots, isolated, _ = amg.mis2(G, 0, 0)
+    agg = amg.aggregate(G, roots, isolated)
+    assert np.all(agg[~isolated] >= 0) and np.all(agg[isolated] == -1)
+    assert np.array_equal(np.sort(np.unique(agg[roots])), np.arange(int(roots.sum())))
+    # each root heads its own aggregate
+    assert np.array_equal(agg[roots], np.arange(int(roots.sum())))
+
+
+def test_tentative_orthonormal_and_reproduces_nullspace(hier):
+    pb, J, H = hier
+    lev = H["levels"][0]
+    Pt = lev["Ptent"].toarray()
+    PtP = Pt.T @ Pt
+    d = np.diag(PtP)
+    keep = d > 0.5  # dropped (singular) columns are zero
+    assert np.allclose(PtP[np.ix_(keep, keep)], np.eye(keep.sum()), atol=1e-13)
+    B = amg.level0_nullspace(pb.n, pb.L)
+    # P_tent B_c = B on aggregated rows (isolated rows are zero rows of P_tent)
+    Pt_s, Bc, _ = amg.tentative(lev["agg"], B, 2)
+    rows = np.repeat(lev["agg"] >= 0, 2)
+    assert np.allclose((Pt_s @ Bc)[rows], B[rows], atol=1e-12)
+
+
+def test_galerkin_operators_spd_and_energy_consistent(hier):
+    pb, J, H = hier
+    rng = np.random.default_rng(0)
+    for l in range(len(H["levels"]) - 1):
+        A, P, Ac = H["levels"][l]["A"], H["levels"][l]["P"], H["levels"][l + 1]["A"]
+        Acd = Ac.toarray()
+        assert np.allclose(Acd, Acd.T, rtol=0, atol=1e-12 * np.abs(Acd).max())
+        assert np.linalg.eigvalsh(0.5 * (Acd + Acd.T)).min() > 0
+        for _ in range(3):
+            xc = rng.standard_normal(Ac.shape[0])
+            xf = P @ xc
+            ef, ec = xf @ (A @ xf), xc @ (Ac @ xc)
+            assert abs(ef - ec) <= 1e-11 * abs(ef)
+
+
+def test_chebyshev_error_polynomial_closed_form():
+    """On a diagonal A with Dinv = I the Chebyshev smoother started from x = 0 gives
+    x = (1 - p(lambda)) b / lambda with p(t) = T_m((th - t)/de) / T_m(th/de) (Saad, Alg. 12.1)."""
+    lam = np.linspace(0.05, 2.0, 40)
+    A = sp.diags(lam).tocsr()
+    lev = {"A": A, "Dinv": sp.identity(lam.size, format="csr"), "lmax": lam.max()}
+    b = np.ones(lam.size)
+    lo, up = 0.03, 1.1
+    for m in (1, 2, 3, 5):
+        x, r = amg.chebyshev(lev, b, None, m, lo, up, need_residual=True)
+        bmax = up * lam.max()
+        amin = lo * bmax
+        th, de = 0.5 * (bmax + amin), 0.5 * (bmax - amin)
+        T = np.polynomial.chebyshev.Chebyshev.basis(m)
+        p = T((th - lam) / de) / T(th / de)
+        assert np.allclose(x, (1.0 - p) / lam, rtol=1e-12, atol=1e-14)
+        assert np.allclose(r, b - lam * x, rtol=1e-12, atol=1e-14)
+
+
+def test_vcycle_symmetric(hier):
+    pb, J, H = hier
+    rng = np.random.default_rng(1)
+    r1, r2 = rng.standard_normal(J.shape[0]), rng.standard_normal(J.shape[0])
+    a, b = amg.vcycle(H, r1) @ r2, r1 @ amg.vcycle(H, r2)
+    assert abs(a - b) <= 1e-11 * max(abs(a), abs(b))
+
+
+def test_single_level_vcycle_is_exact_solve():
+    pb, J = _jacobian(8)
+    H = amg.setup(J, pb, coarse_max_dof=10 ** 6)
+    assert len(H["levels"]) == 1
+    r = np.random.default_rng(2).standard_normal(J.shape[0])
+    x = amg.vcycle(H, r)
+    xd = spla.splu(J.tocsc()).solve(r)
+    assert np.linalg.norm(x - xd) <= 1e-10 * np.linalg.norm(xd)

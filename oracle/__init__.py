@@ -22,9 +22,12 @@ Parity status per function (see DESIGN.md §"Oracle pins"):
   newton.solve_step  pinned (quadratic tail; manufactured solution rate;
                    yield-curve bound; direct vs Krylov solutions)
   krylov.*         pinned (textbook cases, dense solve comparison)
+  transport.*      pinned (zero velocity, textbook 1-D upwind, conservation, Q1 midpoint
+                   face velocities, monotonicity / clamping; tests/test_oracle_transport.py)
   amg.*            pinned for the algebra (Galerkin identity, P_tent
                    orthonormality, near-nullspace reproduction, single-level
-                   exactness, V-cycle symmetry, Chebyshev closed form);
+                   exactness, V-cycle symmetry, Chebyshev closed form, MIS(2)
+                   validity, aggregate partition; tests/test_oracle_amg.py);
                    "parity unpinned" for the hierarchy SHAPE (levels, aggregate
                    counts) — the aggregation is a definition, not a paper result.
 """

@@ -1143,7 +1143,7 @@ __global__ void __launch_bounds__(256) k_cheb_stencil(int n, int Nn, const doubl
 }
 
 // Chebyshev(M) smoothing on the stencil level in one launch (temporal blocking).  A CTA owns
-// a TX x 4 tile of nodes (TX = 34 - 2M, so tile + M-1 rings is 32 nodes = one warp wide) and
+// a TX x FY tile of nodes (TX = 34 - 2M, so tile + M-1 rings is 32 nodes = one warp wide) and
 // one thread per node of the tile plus M-1 rings; each thread keeps its node's stencil row (36
 // values), r and the x increment in registers.  d_0 lives in shared memory on the tile plus M
 // rings: for pre-smoothing (x_0 = 0) it is built in the kernel, r_0 = b, d_0 = ith Dinv b
@@ -1155,13 +1155,13 @@ __global__ void __launch_bounds__(256) k_cheb_stencil(int n, int Nn, const doubl
 // k_resid_dinv_stencil (pre) followed by M k_cheb_stencil launches:
 //   x_M = x_0 + d_0 + ... + d_{M-1};  r_k = r_{k-1} - A d_{k-1};
 //   d_k = c1[k] d_{k-1} + c2[k] Dinv r_k (k < M);  r_M written (out of place) iff pre.
-constexpr int kFW = 32, kFY = 4;  // threads per row (tile + rings), tile rows
+constexpr int kFW = 32;  // threads per row (tile + rings)
 constexpr int kFMaxM = 6;
-template <int M> struct FusedGeom {
+template <int M, int FY> struct FusedGeom {
   static constexpr int R = M - 1;             // rings computed around the tile
   static constexpr int TX = kFW - 2 * R;      // tile width
-  static constexpr int RY = kFY + 2 * R;      // rows of tile + R rings
-  static constexpr int HX = TX + 2 * M, HY = kFY + 2 * M;  // d region (tile + M rings)
+  static constexpr int RY = FY + 2 * R;      // rows of tile + R rings
+  static constexpr int HX = TX + 2 * M, HY = FY + 2 * M;  // d region (tile + M rings)
   static constexpr int NT = kFW * RY;         // threads
 };
 struct ChebFCoef {
@@ -1187,20 +1187,20 @@ __device__ __forceinline__ double2 stencil_apply_reg(bool interior, const double
   return make_double2(y0, y1);
 }
 
-template <int M>
-__global__ void __launch_bounds__(FusedGeom<M>::NT, (FusedGeom<M>::NT <= 256 ? 2 : 1))
+template <int M, int FY>
+__global__ void __launch_bounds__(FusedGeom<M, FY>::NT, (FusedGeom<M, FY>::NT <= 256 ? 2 : 1))
     k_chebM_stencil(int n, int Nn, const double* __restrict__ J, const double* __restrict__ dinv,
                     const double2* __restrict__ rin, const double2* __restrict__ d0g, double2* __restrict__ rout,
                     double2* __restrict__ x, ChebFCoef k, int pre) {
-  using Gm = FusedGeom<M>;
+  using Gm = FusedGeom<M, FY>;
   __shared__ double2 sd[2][Gm::HX * Gm::HY];
   const int s = n + 1;
-  const int i0 = blockIdx.x * Gm::TX, j0 = blockIdx.y * kFY;
+  const int i0 = blockIdx.x * Gm::TX, j0 = blockIdx.y * FY;
   const int t = threadIdx.x;
   const int li = t % kFW, lj = t / kFW;  // position in the tile + R rings
   const int gi = i0 - Gm::R + li, gj = j0 - Gm::R + lj;
   const int di = li < Gm::R ? Gm::R - li : (li >= Gm::TX + Gm::R ? li - (Gm::TX + Gm::R - 1) : 0);
-  const int dj = lj < Gm::R ? Gm::R - lj : (lj >= kFY + Gm::R ? lj - (kFY + Gm::R - 1) : 0);
+  const int dj = lj < Gm::R ? Gm::R - lj : (lj >= FY + Gm::R ? lj - (FY + Gm::R - 1) : 0);
   const int depth = di > dj ? di : dj;  // ring index (0 = tile)
   const bool inside = gi >= 0 && gi <= n && gj >= 0 && gj <= n;
   const int node = gj * s + gi;
@@ -1310,13 +1310,24 @@ __global__ void __launch_bounds__(FusedGeom<M>::NT, (FusedGeom<M>::NT <= 256 ? 2
   }
 }
 
+template <int M, int FY>
+static void launch_chebM_t(Ctx& c, const double* dinv, const double* rin, const double* d0g, double* rout, double* x,
+                           const ChebFCoef& kc, bool pre) {
+  using Gm = FusedGeom<M, FY>;
+  const dim3 grid((c.n + 1 + Gm::TX - 1) / Gm::TX, (c.n + 1 + FY - 1) / FY);
+  k_chebM_stencil<M, FY><<<grid, Gm::NT, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), dinv, (const double2*)rin,
+                                                    (const double2*)d0g, (double2*)rout, (double2*)x, kc, pre ? 1 : 0);
+}
 template <int M>
 static void launch_chebM(Ctx& c, const double* dinv, const double* rin, const double* d0g, double* rout, double* x,
                          const ChebFCoef& kc, bool pre) {
-  using Gm = FusedGeom<M>;
-  const dim3 grid((c.n + 1 + Gm::TX - 1) / Gm::TX, (c.n + 1 + kFY - 1) / kFY);
-  k_chebM_stencil<M><<<grid, Gm::NT, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), dinv, (const double2*)rin,
-                                                (const double2*)d0g, (double2*)rout, (double2*)x, kc, pre ? 1 : 0);
+  // 12 tile rows (16 thread rows incl. the 2 + 2 ring rows, 512 threads, 1 CTA/SM): the ring
+  // recompute drops from 56 % to 42 % of the threads; measured fastest on B200 (config 4: 645 us
+  // per V-cycle vs 679 us at 4 rows, 746 us at 8 rows)
+  static const int fy = getenv("SEAICE_CHEB_FY") ? atoi(getenv("SEAICE_CHEB_FY")) : 12;  // tuning aid
+  if (fy == 12) launch_chebM_t<M, 12>(c, dinv, rin, d0g, rout, x, kc, pre);
+  else if (fy == 8) launch_chebM_t<M, 8>(c, dinv, rin, d0g, rout, x, kc, pre);
+  else launch_chebM_t<M, 4>(c, dinv, rin, d0g, rout, x, kc, pre);
 }
 
 // r = b - A x (or r = b if x == NULL); d = Dinv r * c2 (stencil level)

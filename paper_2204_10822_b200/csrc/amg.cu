@@ -1322,7 +1322,7 @@ template <int M>
 static void launch_chebM(Ctx& c, const double* dinv, const double* rin, const double* d0g, double* rout, double* x,
                          const ChebFCoef& kc, bool pre) {
   // 12 tile rows (16 thread rows incl. the 2 + 2 ring rows, 512 threads, 1 CTA/SM): the ring
-  // recompute drops from 56 % to 42 % of the threads; measured fastest on B200 (config 4: 645 us
+  // recompute drops from 56 % to 34 % of the threads; measured fastest on B200 (config 4: 645 us
   // per V-cycle vs 679 us at 4 rows, 746 us at 8 rows)
   static const int fy = getenv("SEAICE_CHEB_FY") ? atoi(getenv("SEAICE_CHEB_FY")) : 12;  // tuning aid
   if (fy == 12) launch_chebM_t<M, 12>(c, dinv, rin, d0g, rout, x, kc, pre);

@@ -88,6 +88,12 @@ typedef struct {
   int32_t matfree;         /* 0 (default): FGMRES applies the assembled stencil J; 1: FGMRES applies
                               J(v, pi) matrix-free from the (v, pi) of the
                               last assembly, the AMG hierarchy still built from the assembled J */
+  int32_t krylov_forcing;  /* 0 (default): every Newton solve to krylov_rtol (reading G13);
+                              1: Eisenstat-Walker choice-2 forcing (inexact Newton; the paper is
+                              silent on its Krylov tolerance): eta_0 = 0.1, eta_l = 0.9 (|R_l| /
+                              |R_{l-1}|)^2 with the safeguards eta_l >= 0.9 eta_{l-1}^2 (when that
+                              exceeds 0.1) and eta_l >= 0.5 newton_rtol |R_0| / |R_l|, clamped to
+                              [krylov_rtol, 0.1] (reading G29) */
 } seaice_params;
 
 /* Compressed-sparse-row view (scalar rows). Index arrays int32, values fp64. */

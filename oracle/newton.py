@@ -23,7 +23,11 @@ LS_ETA = 1e-12
 
 def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
                ls_max=20, krylov_rtol=1e-8, krylov_maxit=300, restart=30,
-               project_pi=False, amg_params=None, record_iterates=False):
+               project_pi=False, amg_params=None, record_iterates=False, forcing=0):
+    """forcing = 1: Eisenstat-Walker choice 2 for the Krylov tolerance of each solve (reading
+    G29, DESIGN.md): eta_0 = 0.1, eta_l = 0.9 (|R_l|/|R_{l-1}|)^2, safeguards
+    eta_l >= 0.9 eta_{l-1}^2 (if > 0.1) and eta_l >= 0.5 rtol |R_0|/|R_l|, clamped to
+    [krylov_rtol, 0.1]."""
     pb = Problem(inp, prm)
     v = pb.v_prev.copy()
     v[pb.bdof] = 0.0
@@ -48,6 +52,17 @@ def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
             break
         if l == maxit:
             break
+        krtol = krylov_rtol
+        if forcing == 1:
+            eta = 0.1
+            if l > 0:
+                eta = 0.9 * (nr / hist["res"][-2]) ** 2
+                if 0.9 * eta_prev ** 2 > 0.1:
+                    eta = max(eta, 0.9 * eta_prev ** 2)
+            eta = max(eta, 0.5 * rtol * r0 / nr)
+            eta = min(max(eta, krylov_rtol), 0.1)
+            eta_prev = eta
+            krtol = eta
         pi_j = pi if kind == "sv" else None
         J = pb.jacobian(v, pi_j, kind)
         if linsolve == "direct":
@@ -57,12 +72,12 @@ def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
             vt = krylov.dense_cholesky_solve(J, R)
             kst = {"iters": 0}
         elif linsolve == "jacobi_fgmres":
-            vt, kst = krylov.fgmres(lambda x: J @ x, R, krylov.jacobi(J), restart, krylov_rtol, krylov_maxit)
+            vt, kst = krylov.fgmres(lambda x: J @ x, R, krylov.jacobi(J), restart, krtol, krylov_maxit)
         elif linsolve == "amg_fgmres":
             from . import amg
             H = amg.setup(J, pb, **(amg_params or {}))
             vt, kst = krylov.fgmres(lambda x: J @ x, R, lambda r: amg.vcycle(H, r), restart,
-                                    krylov_rtol, krylov_maxit)
+                                    krtol, krylov_maxit)
             kst["levels"] = len(H["levels"])
         else:
             raise ValueError(linsolve)

@@ -68,6 +68,7 @@ void validate(const seaice_params* p) {
   SI_CHECK(p->cheb_fused == 0 || p->cheb_fused == 1, SEAICE_EINVAL, "cheb_fused must be 0 or 1");
   SI_CHECK(p->cheb_degree0 >= 0 && p->cheb_degree0 <= 16, SEAICE_EINVAL, "cheb_degree0 in [0,16]");
   SI_CHECK(p->matfree == 0 || p->matfree == 1, SEAICE_EINVAL, "matfree must be 0 or 1");
+  SI_CHECK(p->krylov_forcing == 0 || p->krylov_forcing == 1, SEAICE_EINVAL, "krylov_forcing must be 0 or 1");
 }
 
 int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* out) {
@@ -102,12 +103,33 @@ int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* o
     st.amg_levels = c.nlev;
     st.amg_op_complexity = c.op_complexity;
   }
-  // a-5: J vt = R
+  // a-5: J vt = R (to krylov_rtol, or to the Eisenstat-Walker forcing term, reading G29)
   c.vt.ensure(c.al, c.N);
   int kst;
   {
     EvTimer t(c);
-    kst = fgmres_impl(c, c.R.get(), c.vt.get(), &st.krylov);
+    const double rtol_fixed = c.p.krylov_rtol;
+    if (c.p.krylov_forcing == 1) {
+      double eta = 0.1;
+      if (c.ew_prev_res > 0.0) {
+        const double ratio = st.res_norm / c.ew_prev_res;
+        eta = 0.9 * ratio * ratio;
+        const double sg = 0.9 * c.ew_prev_eta * c.ew_prev_eta;
+        if (sg > 0.1) eta = std::max(eta, sg);
+      }
+      eta = std::max(eta, 0.5 * c.p.newton_rtol * c.r0 / st.res_norm);
+      eta = std::min(std::max(eta, rtol_fixed), 0.1);
+      c.ew_prev_res = st.res_norm;
+      c.ew_prev_eta = eta;
+      c.p.krylov_rtol = eta;
+    }
+    try {
+      kst = fgmres_impl(c, c.R.get(), c.vt.get(), &st.krylov);
+    } catch (...) {
+      c.p.krylov_rtol = rtol_fixed;
+      throw;
+    }
+    c.p.krylov_rtol = rtol_fixed;
     st.t_krylov = t.ms();
   }
   // a-6: backtracking on Phi, difference form
@@ -232,6 +254,7 @@ void seaice_default_params(seaice_params* p, int32_t n) {
   p->cheb_fused = 1;
   p->cheb_degree0 = 0;  // measured no gain on B200 (grid barriers ~ launch gaps in the graph)
   p->matfree = 0;       // the assembled 19-value stencil SpMV is ~4x cheaper than the matrix-free apply
+  p->krylov_forcing = 0;  // fixed krylov_rtol per Newton solve (reading G13)
 }
 
 int seaice_create(const seaice_params* p, const seaice_runtime* rt, seaice_ctx** out) {

@@ -429,6 +429,8 @@ void set_step_impl(Ctx& c, double dt, double t_new, const double* h, const doubl
   c.assembled = false;
   c.amg_ready = false;
   c.have_r0 = false;
+  c.ew_prev_res = 0.0;
+  c.ew_prev_eta = 0.0;
 }
 
 // ------------------------------------------------------------------ K1, fused residual + Jacobian

@@ -153,6 +153,7 @@ struct Ctx {
   // Newton
   bool have_r0 = false;
   double r0 = 0.0;
+  double ew_prev_res = 0.0, ew_prev_eta = 0.0;  // Eisenstat-Walker state of the current step
   DBuf<double> vt, pit;
 
   // Krylov

@@ -11,7 +11,7 @@ kernels use an orthonormal 3-vector basis.  Only `paper_2204_10822_b200.workload
 Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s cpu_baseline /
 `--impl reference` legs may import this package.  The product path never does.
 
-Parity status per function (see DESIGN.md §"Oracle pins"):
+Parity status per function (see DESIGN.md §13 "Oracle pins"):
   fem.*            pinned (closed-form Q1 tables, mass matrix, quadrature exactness)
   model.residual   pinned (Phi' = -R by FD; worked example; vanishing cases)
   model.energy /

@@ -135,6 +135,11 @@ typedef struct {
   int32_t newton_iters, converged, krylov_iters_total;
   double res_norm0, res_norm_final, seconds;
   double t_assemble, t_amg, t_krylov, t_ls, t_setup; /* milliseconds */
+  int32_t krylov_solves;    /* linear solves in the step (= newton_iters) */
+  int32_t krylov_capped;    /* solves that stopped at krylov_maxit without reaching krylov_rtol
+                               (their iterations are counted in krylov_iters_total; the Newton
+                               step still used the capped iterate) */
+  int32_t krylov_max_iters; /* largest iteration count of one solve */
 } seaice_step_stats;
 
 /* Default parameters (Table 1 + BASELINE.json + DESIGN.md readings) for mesh size n. */
@@ -172,16 +177,21 @@ int seaice_assemble_jacobian(seaice_ctx* ctx, const double* v, const double* pi,
 /* y = J x with the last assembled Jacobian. */
 int seaice_spmv(seaice_ctx* ctx, const double* x, double* y);
 
-/* Explicit transport of A and H between momentum steps: one explicit-Euler,
- * first-order upwind finite-volume step of eq:model:A / eq:model:H ("an explicit
+/* Explicit transport of A and H between momentum steps: explicit-Euler,
+ * first-order upwind finite-volume steps of eq:model:A / eq:model:H ("an explicit
  * time step (e.g., an explicit Euler step)"; scheme = DESIGN.md reading G28).
  * v: nodal velocity [2(n+1)^2] interleaved (device); A, H: cell fields [n*n] row-major
  * (device, read); A_out, H_out: [n*n] (device, written; must not alias A or H).  Face-normal
  * velocity = mean of the face's two nodal velocities; an inflow boundary face carries A_in /
- * H_in; A_out is clamped to [0,1], H_out to [0,inf).  Enqueued on the ctx stream,
- * no synchronisation.  EINVAL on NULL / aliased buffers or dt < 0 / non-finite. */
+ * H_in; A_out is clamped to [0,1], H_out to [0,inf).
+ * CFL guard: CFL = max over cells of dt/dx * (sum of the cell's outflow face velocities), the
+ * bound under which the upwind update is monotone.  If CFL > 1 the step is taken as
+ * m = ceil(CFL) sub-steps of dt/m (same v).  *cfl_host and *substeps_host (each may be NULL)
+ * receive CFL and m.  Synchronises the ctx stream once (to read CFL).  EINVAL on NULL /
+ * aliased buffers, dt < 0 / non-finite or CFL > 1e5; ENONFINITE on a non-finite velocity. */
 int seaice_transport(seaice_ctx* ctx, double dt, const double* v, const double* A, const double* H,
-                     double A_in, double H_in, double* A_out, double* H_out);
+                     double A_in, double H_in, double* A_out, double* H_out, double* cfl_host,
+                     int32_t* substeps_host);
 
 /* Matrix-free Jacobian apply y = J(v, pi) x (eq:linearSVNewton P:512-525 with
  * eq:modification P:534-539; the JFNK discussion P:545-653): the element matrices of the ctx's
@@ -219,7 +229,10 @@ int seaice_pi_tilde(seaice_ctx* ctx, const double* v, const double* pi, const do
 int seaice_get_pi(seaice_ctx* ctx, double* pi_out);
 int seaice_set_pi(seaice_ctx* ctx, const double* pi_in);
 
-/* One Newton iteration.  The first call after set_step
+/* One Newton iteration of the stress-velocity method: v_{l+1} = v_l + alpha v~,
+ * pi_{l+1} = pi_l + alpha pi~ with J(v_l, pi_l) v~ = R(v_l) (eq:linearSVNewton
+ * P:512-527, eq:modification P:534-539) and alpha from backtracking on Phi (P:355-360,
+ * P:727-732; difference form, reading G12/G12b).  The first call after set_step
  * records r0 = ||R(v)||; a call that finds ||R(v)|| <= newton_rtol*r0 (or r0 < 1e-14)
  * sets converged_on_entry = 1 and takes no step.  Otherwise: assemble, (AMG setup),
  * FGMRES, energy backtracking, v += alpha v~, pi += alpha pi~.  pi_inout may be
@@ -227,7 +240,9 @@ int seaice_set_pi(seaice_ctx* ctx, const double* pi_in);
 int seaice_newton_step(seaice_ctx* ctx, double* v_inout, double* pi_inout, seaice_newton_stats* st);
 
 /* Whole implicit step: set_step + Newton loop to convergence; v_out [N] device.
- * NOT_CONVERGED if newton_maxit is reached. */
+ * NOT_CONVERGED if newton_maxit is reached.  Linear solves that hit krylov_maxit do not
+ * change the return code (Newton tolerates inexact solves) but are counted in
+ * st->krylov_capped. */
 int seaice_solve_step(seaice_ctx* ctx, double dt, double t_new, const double* h, const double* A,
                       const double* v_prev, const double* v_air, const double* v_ocean, double* v_out,
                       seaice_step_stats* st);

@@ -9,8 +9,10 @@ G13): rtol 1e-8 relative to ||b||, restart 30, maxit 300.
 FGMRES definition shared (as a definition, not code) with the CUDA path:
 right preconditioning, x0 = 0, classical Gram-Schmidt (one pass, PETSc's
 default), Givens rotations, inner stop when |g_{j+1}| <= rtol ||b||, explicit
-residual r = b - A x at every restart; the iteration count is the total number
-of preconditioned matrix-vector products.
+residual r = b - A x at every restart; converged only when that explicit residual
+satisfies ||r|| <= rtol ||b|| (an estimate below tol with a larger true residual --
+loss of orthogonality in one-pass CGS -- restarts); the iteration count is the total
+number of preconditioned matrix-vector products.
 """
 from __future__ import annotations
 
@@ -72,7 +74,7 @@ def fgmres(Aop, b, Mop=None, restart=30, rtol=1e-8, maxit=300):
         r = b - Aop(x)
         beta = float(np.linalg.norm(r))
         stats["relres_est"] = est / bnorm
-        if beta <= rtol * bnorm or est <= rtol * bnorm:
+        if beta <= rtol * bnorm:
             break
         if its >= maxit:
             stats["converged"] = False

@@ -75,9 +75,28 @@ def advect_step(q: np.ndarray, ux: np.ndarray, uy: np.ndarray, dt: float, dx: fl
     return out.ravel()
 
 
+def cfl_number(ux: np.ndarray, uy: np.ndarray, dt: float, dx: float) -> float:
+    """max over cells of dt/dx * (sum of the cell's outflow face velocities).  The upwind update
+    q' = q (1 - dt/dx out) + dt/dx sum_in u q_nb is a convex combination (monotone) iff this
+    is <= 1 (the 2-D upwind CFL condition)."""
+    n = ux.shape[0]
+    worst = 0.0
+    for j in range(n):
+        for i in range(n):
+            out = max(-ux[j, i], 0.0) + max(ux[j, i + 1], 0.0) + max(-uy[j, i], 0.0) + max(uy[j + 1, i], 0.0)
+            worst = max(worst, dt / dx * out)
+    return worst
+
+
 def transport_step(v: np.ndarray, A: np.ndarray, H: np.ndarray, n: int, dt: float, dx: float,
-                   A_in: float = 1.0, H_in: float = 0.0):
-    """A^{n+1}, H^{n+1} from (v^n, A^n, H^n) (P:244-248): A in [0, 1], H >= 0."""
+                   A_in: float = 1.0, H_in: float = 0.0, info: bool = False):
+    """A^{n+1}, H^{n+1} from (v^n, A^n, H^n) (P:244-248): A in [0, 1], H >= 0.
+    CFL guard (reading G28): if cfl_number > 1 the step is m = ceil(CFL) sub-steps of dt/m
+    with the same v.  info=True also returns (cfl, m)."""
     ux, uy = face_velocities(v, n)
-    return (advect_step(A, ux, uy, dt, dx, A_in, 0.0, 1.0),
-            advect_step(H, ux, uy, dt, dx, H_in, 0.0, None))
+    cfl = cfl_number(ux, uy, dt, dx)
+    m = int(np.ceil(cfl)) if cfl > 1.0 else 1
+    for _ in range(m):
+        A, H = (advect_step(A, ux, uy, dt / m, dx, A_in, 0.0, 1.0),
+                advect_step(H, ux, uy, dt / m, dx, H_in, 0.0, None))
+    return (A, H, cfl, m) if info else (A, H)

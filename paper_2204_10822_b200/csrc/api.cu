@@ -1,4 +1,5 @@
 // api.cu — the extern "C" boundary (include/seaice.h) and the Newton driver.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -203,6 +204,9 @@ int solve_step_impl(Ctx& c, double dt, double t_new, const double* h, const doub
     }
     st.newton_iters++;
     st.krylov_iters_total += ns.krylov.iters;
+    st.krylov_solves++;
+    if (!ns.krylov.converged) st.krylov_capped++;
+    st.krylov_max_iters = std::max(st.krylov_max_iters, ns.krylov.iters);
     st.t_amg += ns.t_amg;
     st.t_krylov += ns.t_krylov;
     st.t_ls += ns.t_ls;
@@ -367,9 +371,11 @@ int seaice_spmv(seaice_ctx* h, const double* x, double* y) {
 }
 
 int seaice_transport(seaice_ctx* h, double dt, const double* v, const double* A, const double* H, double A_in,
-                     double H_in, double* A_out, double* H_out) {
+                     double H_in, double* A_out, double* H_out, double* cfl_host, int32_t* substeps_host) {
   API_BEGIN(h)
-  transport_impl(c, dt, v, A, H, A_in, H_in, A_out, H_out);
+  int m = 1;
+  transport_impl(c, dt, v, A, H, A_in, H_in, A_out, H_out, cfl_host, &m);
+  if (substeps_host) *substeps_host = m;
   return SEAICE_OK;
   API_END
 }

@@ -247,7 +247,7 @@ void set_step_impl(Ctx& c, double dt, double t_new, const double* h, const doubl
 void assemble_impl(Ctx& c, const double* v, const double* pi, bool jacobian, double* r_out, double* norm_host);
 void jv_matfree_impl(Ctx& c, const double* v, const double* pi, const double* x, double* y);
 void transport_impl(Ctx& c, double dt, const double* v, const double* A, const double* H, double A_in, double H_in,
-                    double* Ao, double* Ho);
+                    double* Ao, double* Ho, double* cfl_out = nullptr, int* substeps_out = nullptr);
 void build_csr_view(Ctx& c, seaice_csr* out);
 void delta_energy_impl(Ctx& c, const double* v, const double* vt, const double* alphas, int count, double* out,
                        double* sabs = nullptr);

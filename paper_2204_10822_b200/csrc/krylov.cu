@@ -1,7 +1,8 @@
 // krylov.cu — right-preconditioned FGMRES(m) driven from the host.
 // Definition shared with oracle/krylov.py (as a definition, not code): x0 = 0,
-// classical Gram-Schmidt in one pass, Givens rotations, stop when the estimate
-// |g_{j+1}| <= rtol ||b||, explicit residual at every restart.
+// classical Gram-Schmidt in one pass, Givens rotations, the inner loop stops when the
+// estimate |g_{j+1}| <= rtol ||b||; convergence is declared only when the explicit residual
+// computed at the end of the cycle satisfies ||b - A x|| <= rtol ||b|| (else restart).
 #include <cmath>
 #include <vector>
 
@@ -127,7 +128,7 @@ int fgmres_impl(Ctx& c, const double* b, double* x, seaice_krylov_stats* st) {
     beta = norm2(c, c.rk.get(), N);
     r = c.rk.get();
     S.relres_est = est / bnorm;
-    if (beta <= tol || est <= tol) {
+    if (beta <= tol) {
       converged = true;
       break;
     }

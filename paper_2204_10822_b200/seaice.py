@@ -73,7 +73,8 @@ class StepStats(C.Structure):
     _fields_ = [("newton_iters", C.c_int32), ("converged", C.c_int32), ("krylov_iters_total", C.c_int32),
                 ("res_norm0", C.c_double), ("res_norm_final", C.c_double), ("seconds", C.c_double),
                 ("t_assemble", C.c_double), ("t_amg", C.c_double), ("t_krylov", C.c_double), ("t_ls", C.c_double),
-                ("t_setup", C.c_double)]
+                ("t_setup", C.c_double), ("krylov_solves", C.c_int32), ("krylov_capped", C.c_int32),
+                ("krylov_max_iters", C.c_int32)]
 
 
 def struct_dict(s):
@@ -124,7 +125,7 @@ def lib(build_if_missing: bool = True):
             "seaice_residual": (C.c_int, [VP, VP, VP, P(D)]),
             "seaice_assemble_jacobian": (C.c_int, [VP, VP, VP, P(CSR)]),
             "seaice_spmv": (C.c_int, [VP, VP, VP]),
-            "seaice_transport": (C.c_int, [VP, D, VP, VP, VP, D, D, VP, VP]),
+            "seaice_transport": (C.c_int, [VP, D, VP, VP, VP, D, D, VP, VP, P(D), P(I32)]),
             "seaice_jv_matfree": (C.c_int, [VP, VP, VP, VP, VP]),
             "seaice_amg_setup": (C.c_int, [VP, P(I32), P(D)]),
             "seaice_amg_level": (C.c_int, [VP, I32, P(BSR), P(BSR), VP]),
@@ -402,12 +403,15 @@ class SeaIce:
         self._check(self.L.seaice_jv_matfree(self.h, _ptr(v), _ptr(pi), _ptr(x), _ptr(y)))
         return y
 
-    def transport(self, dt, v, A, h, A_in=1.0, h_in=0.0):
-        """(A, h) advanced by one explicit upwind step with velocity v (seaice_transport)."""
+    def transport(self, dt, v, A, h, A_in=1.0, h_in=0.0, info=False):
+        """(A, h) advanced over dt by explicit upwind steps with velocity v (seaice_transport;
+        sub-cycled when the CFL number exceeds 1).  info=True also returns (cfl, substeps)."""
         v, A, h = self.tensor(v, self.N), self.tensor(A, self.Nc), self.tensor(h, self.Nc)
         Ao, ho = self.zeros(self.Nc), self.zeros(self.Nc)
-        self._check(self.L.seaice_transport(self.h, dt, _ptr(v), _ptr(A), _ptr(h), A_in, h_in, _ptr(Ao), _ptr(ho)))
-        return Ao, ho
+        cfl, m = C.c_double(), C.c_int32()
+        self._check(self.L.seaice_transport(self.h, dt, _ptr(v), _ptr(A), _ptr(h), A_in, h_in, _ptr(Ao), _ptr(ho),
+                                            C.byref(cfl), C.byref(m)))
+        return (Ao, ho, cfl.value, m.value) if info else (Ao, ho)
 
     def solve_step_host(self, dt, t_new, h, A, v_prev, v_air, v_ocean, v_out):
         """Host (CPU, ideally pinned) torch tensors in and out: the end-to-end call."""

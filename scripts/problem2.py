@@ -33,13 +33,16 @@ for run in a.runs.split(","):
     h0, A0, v0 = wl.problem2_initial(n)
     vo = torch.as_tensor(wl.ocean_nodal(n), device="cuda")
     h, A, v = (torch.as_tensor(x, device="cuda") for x in (h0, A0, v0))
-    newton, krylov, secs, tsec, conv = [], [], [], [], 0
+    newton, krylov, secs, tsec, conv, cfls, subs = [], [], [], [], 0, [], []
+    ctx_capped = 0
     for k in range(steps):
         t_new = (k + 1) * dt
         va = torch.as_tensor(wl.problem2_wind_nodal(n, t_new), device="cuda")
         torch.cuda.synchronize()
         t0 = time.time()
-        A, h = ctx.transport(dt, v, A, h)
+        A, h, cfl, msub = ctx.transport(dt, v, A, h, info=True)
+        cfls.append(cfl)
+        subs.append(msub)
         torch.cuda.synchronize()
         t1 = time.time()
         v, st = ctx.solve_step(dt, t_new, h, A, v, va, vo)
@@ -50,14 +53,16 @@ for run in a.runs.split(","):
         secs.append(t2 - t1)
         tsec.append(t1 - t0)
         conv += st["converged"]
+        ctx_capped += st["krylov_capped"]
         if a.per_step:
             print(json.dumps({"n": n, "step": k + 1, "day": t_new / wl.DAY, "newton": st["newton_iters"],
-                              "krylov": st["krylov_iters_total"], "seconds": round(t2 - t1, 4),
+                              "krylov": st["krylov_iters_total"], "seconds": round(t2 - t1, 4), "cfl": cfl,
                               "A_min": float(A.min()), "h_max": float(h.max())}), flush=True)
     rec = {"problem": "II", "n": n, "dx_km": 512.0 / n, "dof": ctx.N, "steps": steps, "days": steps * dt / wl.DAY,
            "converged_steps": conv, "newton_mean": statistics.mean(newton), "newton_max": max(newton),
            "krylov_per_solve": sum(krylov) / max(sum(newton), 1), "s_per_step": statistics.mean(secs),
-           "transport_us_per_step": 1e6 * statistics.median(tsec),
+           "transport_us_per_step": 1e6 * statistics.median(tsec), "cfl_max": max(cfls),
+           "transport_substeps_max": max(subs), "krylov_capped": ctx_capped,
            "paper_newton_mean_8d": PAPER_NEWTON.get(n), "paper_krylov_per_solve_8d": PAPER_KRYLOV.get(n),
            "A_min": float(A.min()), "A_max": float(A.max()), "h_min": float(h.min()), "h_max": float(h.max())}
     print(json.dumps(rec), flush=True)

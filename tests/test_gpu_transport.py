@@ -35,6 +35,25 @@ def test_transport_kernel_parity(n):
     assert Ag.min() >= 0.0 and Ag.max() <= 1.0 and Hg.min() >= 0.0
 
 
+@pytest.mark.parametrize("n,courant", [(37, 2.6), (64, 7.3)])
+def test_transport_cfl_guard_subcycles_like_oracle(n, courant):
+    """CFL > 1 (0.5 km Problem II at dt = 1800 s exceeds it above 0.28 m/s): both sides
+    report the same Courant number, take ceil(CFL) sub-steps and agree to rounding; the result
+    stays in [0, 1] without relying on the clamp (monotone sub-steps)."""
+    rng = np.random.default_rng(n)
+    dx = wl.L_DOMAIN / n
+    v = rng.normal(0.0, 0.3, 2 * (n + 1) ** 2)
+    A = rng.uniform(0.2, 0.9, n * n)
+    H = rng.uniform(0.0, 0.05, n * n)
+    ux, uy = T.face_velocities(v, n)
+    dt = courant / T.cfl_number(ux, uy, 1.0, dx)
+    Ao, Ho, cflo, mo = T.transport_step(v, A, H, n, dt, dx, A_in=0.5, H_in=0.01, info=True)
+    ctx = make_ctx(n)
+    Ag, Hg, cflg, mg = ctx.transport(dt, v, A, H, A_in=0.5, h_in=0.01, info=True)
+    assert mg == mo == int(np.ceil(courant - 1e-12)) and abs(cflg - cflo) <= 1e-14 * cflo
+    assert np.max(np.abs(Ag.cpu().numpy() - Ao)) <= 1e-13 and np.max(np.abs(Hg.cpu().numpy() - Ho)) <= 1e-14
+
+
 def test_transport_rejects_aliasing_and_negative_dt():
     from paper_2204_10822_b200.seaice import SeaIceError
     n = 8
@@ -43,7 +62,7 @@ def test_transport_rejects_aliasing_and_negative_dt():
     A = torch.ones(n * n, dtype=torch.float64, device="cuda")
     H = torch.ones(n * n, dtype=torch.float64, device="cuda")
     from paper_2204_10822_b200.seaice import _ptr
-    rc = ctx.L.seaice_transport(ctx.h, 1.0, _ptr(v), _ptr(A), _ptr(H), 1.0, 0.0, _ptr(A), _ptr(H))
+    rc = ctx.L.seaice_transport(ctx.h, 1.0, _ptr(v), _ptr(A), _ptr(H), 1.0, 0.0, _ptr(A), _ptr(H), None, None)
     assert rc == -1  # SEAICE_EINVAL
     with pytest.raises(SeaIceError):
         ctx.transport(-1.0, v, A, H)

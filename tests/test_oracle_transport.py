@@ -96,3 +96,27 @@ def test_uniform_diagonal_velocity_is_monotone_and_clamps():
     v = wl.random_velocity(n, 6, amp=5.0)
     A1, H1 = T.transport_step(v, A, np.full(n * n, 1e-3), n, 600.0, 1.0e3)
     assert A1.min() >= 0.0 and A1.max() <= 1.0 and H1.min() >= 0.0
+
+
+def test_cfl_number_closed_form_and_subcycling():
+    """Uniform v = (u, w), u, w > 0: every cell's outflow is u + w, so CFL = dt (u + w)/dx; with
+    CFL = 2.5 the step is ceil(2.5) = 3 textbook upwind sub-steps of dt/3 (1-D check in x with
+    w = 0: c <- c - (u dt/3dx)(c - c_left) three times)."""
+    n, dx, u, w = 8, 1.0e3, 1.5, 1.0
+    v = np.zeros(2 * (n + 1) ** 2)
+    v[0::2], v[1::2] = u, w
+    ux, uy = T.face_velocities(v, n)
+    assert abs(T.cfl_number(ux, uy, 400.0, dx) - 400.0 * (u + w) / dx) <= 1e-15
+    v[1::2] = 0.0
+    dt = 2.5 * dx / u
+    rng = np.random.default_rng(7)
+    A = rng.uniform(0.2, 0.8, n * n)
+    A1, H1, cfl, m = T.transport_step(v, A, A.copy(), n, dt, dx, A_in=0.4, H_in=0.4, info=True)
+    assert m == 3 and abs(cfl - 2.5) <= 1e-15
+    Q = A.reshape(n, n).copy()
+    c = u * dt / 3 / dx
+    for _ in range(3):
+        left = np.concatenate([np.full((n, 1), 0.4), Q[:, :-1]], axis=1)
+        Q = Q - c * (Q - left)
+    assert np.max(np.abs(A1 - Q.ravel())) <= 1e-15 and np.max(np.abs(H1 - Q.ravel())) <= 1e-15
+    assert A1.min() >= 0.2 - 1e-15 and A1.max() <= 0.8 + 1e-15   # monotone: no clamp needed

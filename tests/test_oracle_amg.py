@@ -119,3 +119,45 @@ def test_single_level_vcycle_is_exact_solve():
     x = amg.vcycle(H, r)
     xd = spla.splu(J.tocsc()).solve(r)
     assert np.linalg.norm(x - xd) <= 1e-10 * np.linalg.norm(xd)
+
+
+def _block_eigs_DinvA(J, b):
+    """Eigenvalues of D^-1 A (D = b x b block diagonal) by a dense generalized symmetric
+    eigen-solve A x = lambda D x (A, D SPD): scipy.linalg.eigh, independent of the oracle."""
+    import scipy.linalg as sla
+    A = J.toarray()
+    D = np.zeros_like(A)
+    for I in range(A.shape[0] // b):
+        s = slice(b * I, b * I + b)
+        D[s, s] = A[s, s]
+    return sla.eigh(A, D, eigvals_only=True)
+
+
+@pytest.mark.parametrize("n,seed", [(8, 3), (12, 4)])
+def test_lambda_max_power_iteration_vs_eigensolve(n, seed):
+    """lambda_max (20 power iterations on D^-1 A from the seeded start) lies within
+    [0.9, 1.0] x the largest eigenvalue of the pencil (A, D) from a dense eigen-solve.  It feeds
+    omega = 4/(3 lambda) and the Chebyshev interval [lo b, b], b = 1.1 lambda."""
+    pb, J = _jacobian(n, seed=seed)
+    Dinv, _ = amg.block_diag_inv(J, 2)
+    lam = amg.lambda_max(J, Dinv, 0, 0, 20)
+    ev = _block_eigs_DinvA(J, 2)
+    assert 0.9 * ev.max() <= lam <= 1.0 * ev.max() * (1 + 1e-12), (lam, ev.max())
+
+
+def test_strength_threshold_hand_example():
+    """DESIGN §5 strength: blocks I != J strong iff ||A_IJ||_F^2 >= theta^2 ||A_II||_F ||A_JJ||_F.
+    Three nodes, A_00 = 2 I, A_11 = 8 I, A_22 = 8 I, A_01 = c I, A_12 = 0.5 I: ||A_01||^2 = 2 c^2
+    against theta^2 * (2 sqrt2)(8 sqrt2) = 32 theta^2, so with theta = 0.25 the pair (0,1) is
+    strong iff c >= 1 (checked just above and below); (1,2): 2 * 0.25 = 0.5 < 0.0625 * 128 = 8, weak.
+    The stored strength value is s_IJ = ||A_IJ||^2 / (||A_II|| ||A_JJ||)."""
+    for c, strong in ((1.001, True), (0.999, False), (1.3, True)):
+        blocks = {(0, 0): 2.0, (1, 1): 8.0, (2, 2): 8.0, (0, 1): c, (1, 0): c, (1, 2): 0.5, (2, 1): 0.5}
+        A = np.zeros((6, 6))
+        for (I, K), s in blocks.items():
+            A[2 * I:2 * I + 2, 2 * K:2 * K + 2] = s * np.eye(2)
+        G = amg.strength(sp.csr_matrix(A), 2, 0.25).toarray()
+        assert (G[0, 1] > 0) == strong and (G[1, 0] > 0) == strong
+        assert G[1, 2] == 0 and G[2, 1] == 0
+        if strong:
+            assert abs(G[0, 1] - 2 * c * c / 32.0) <= 1e-15

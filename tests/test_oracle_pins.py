@@ -485,3 +485,44 @@ def test_newton_krylov_paths_agree():
                                   krylov_rtol=1e-11, krylov_maxit=20000)
     assert abs(h1["newton_iters"] - h2["newton_iters"]) <= 1
     assert np.linalg.norm(v1 - v2) <= 1e-7 * np.linalg.norm(v1)
+
+
+# ------------------------------------------------------------------ Coriolis (round-2 pins)
+def test_e_r_cross_right_hand_rule():
+    """e_r is the upward unit normal: e_r x e_x = e_y and e_r x e_y = -e_x
+    (right-hand rule z^ x x^ = y^, z^ x y^ = -x^)."""
+    assert np.array_equal(M.e_r_cross(np.array([1.0, 0.0])), np.array([0.0, 1.0]))
+    assert np.array_equal(M.e_r_cross(np.array([0.0, 1.0])), np.array([-1.0, 0.0]))
+
+
+def test_worked_example_2x2_coriolis_and_drag():
+    """Hand derivation on the 2x2-cell mesh (single interior node c), v = 0, uniform h, A = 1,
+    v^n = (a, b) on every node (so v^n != v_o), uniform v_o = (u_o, w_o) and uniform tau_atm.
+    Every integrand of eq:F and of the ocean term of eq:A is then a
+    constant times N_c, int N_c = dx^2 (exact under 2x2 Gauss), the pressure term cancels for
+    uniform P, and the viscous term vanishes at v = 0, so
+        R_c = dx^2 [rho h v^n - dt rho h f_c e_r x (v^n - v_o) + dt tau_atm + dt C_o rho_o |v_o| v_o]
+    with e_r x (x, y) = (-y, x).  A sign flip of the Coriolis term (in F or in e_r x) moves R_c by
+    2 dt rho h f_c dx^2 |v^n - v_o| ~ 1e-3 relative, far above the 1e-12 tolerance."""
+    n, dx, h, dt = 2, 16.0e3, 0.3, 1800.0
+    L = n * dx
+    Nn = (n + 1) ** 2
+    a, b = 0.12, -0.05
+    uo, wo = -0.3, 0.2
+    ta = np.array([0.2, -0.1])
+    speed = math.sqrt(np.linalg.norm(ta) / (PRM.C_a * PRM.rho_a))
+    va = speed * ta / np.linalg.norm(ta)
+    inp = wl.StepInputs(n=n, dt=dt, t_new=dt, h=np.full(n * n, h), A=np.ones(n * n),
+                        v_prev=np.tile([a, b], Nn), v_air=np.tile(va, Nn), v_ocean=np.tile([uo, wo], Nn), L=L)
+    pb = M.Problem(inp, PRM)
+    R = pb.residual(np.zeros(pb.N))
+    rh, f = PRM.rho_i * h, PRM.f_c
+    dvx, dvy = a - uo, b - wo
+    cor = np.array([-dvy, dvx])                       # e_r x (v^n - v_o)
+    wo_vec = np.array([uo, wo])
+    expect = dx * dx * (rh * np.array([a, b]) - dt * rh * f * cor + dt * ta
+                        + dt * PRM.C_o * PRM.rho_o * np.linalg.norm(wo_vec) * wo_vec)
+    c = 4
+    assert np.allclose(R[2 * c:2 * c + 2], expect, rtol=1e-12, atol=0.0)
+    flipped = expect + 2 * dx * dx * dt * rh * f * cor
+    assert np.min(np.abs(R[2 * c:2 * c + 2] - flipped)) > 1e-6 * np.max(np.abs(expect))

@@ -94,6 +94,13 @@ typedef struct {
                               |R_{l-1}|)^2 with the safeguards eta_l >= 0.9 eta_{l-1}^2 (when that
                               exceeds 0.1) and eta_l >= 0.5 newton_rtol |R_0| / |R_l|, clamped to
                               [krylov_rtol, 0.1] (reading G29) */
+  int32_t nullspace_dim;   /* AMG near-nullspace columns per aggregate = coarse block size:
+                              3 = rigid-body modes (1,0), (0,1), rotation; 4 (reading G30)
+                              adds the linearisation point v_l of the last seaice_assemble_jacobian,
+                              a near-null vector of the plastic part of eq:modification:
+                              C_q tau(v_l) = (P/Delta)(Delta_min^2/Delta^2) tau(v_l) at consistent pi */
+  int32_t krylov_method;   /* 0 (default): FGMRES(restart); 1: preconditioned CG (J and the
+                              symmetric V-cycle are SPD, eq:modification P:534-539; same stopping test) */
 } seaice_params;
 
 /* Compressed-sparse-row view (scalar rows). Index arrays int32, values fp64. */

@@ -23,7 +23,8 @@ Definition (every choice is a parameter; both sides implement it independently):
   P_tent     per aggregate (members in index order) modified Gram-Schmidt, two projection
              passes, of the stacked near-nullspace rows; a column whose remaining norm is
              <= 1e-8 of its original norm is dropped (zero column); B_c = R.
-             Level-0 near-nullspace: (1,0), (0,1), (-(y - L/2), x - L/2)/L per node.
+             Level-0 near-nullspace: (1,0), (0,1), (-(y - L/2), x - L/2)/L per node, and with
+             nullspace_dim = 4 (reading G30) the linearisation point v_l as a fourth column.
   smoothing  P = P_tent - omega D^-1 A P_tent, omega = 4/(3 lambda), D = block diagonal.
   lambda     power iteration on D^-1 A, `power_iters` steps from x0_i = uniform[-1,1) drawn
              by splitmix64(i + GOLDEN*(64 seed + level + 7)); lambda = ||D^-1 A x|| for ||x|| = 1.
@@ -155,11 +156,11 @@ def aggregate(G, roots, isolated):
 
 
 def mgs_qr(Bs, tol=1e-8):
-    """Two-pass modified Gram-Schmidt with column dropping; returns Q (m x 3), R (3 x 3)."""
-    m = Bs.shape[0]
-    Q = np.zeros((m, 3))
-    R = np.zeros((3, 3))
-    for k in range(3):
+    """Two-pass modified Gram-Schmidt with column dropping; returns Q (m x k), R (k x k)."""
+    m, kk = Bs.shape
+    Q = np.zeros((m, kk))
+    R = np.zeros((kk, kk))
+    for k in range(kk):
         v = Bs[:, k].copy()
         n0 = np.sqrt(v @ v)
         for _ in range(2):
@@ -176,9 +177,10 @@ def mgs_qr(Bs, tol=1e-8):
 
 def tentative(agg, B, b):
     nb = agg.size
+    K = B.shape[1]
     na = int(agg.max()) + 1 if agg.size and agg.max() >= 0 else 0
     rows, cols, vals = [], [], []
-    Bc = np.zeros((3 * na, 3))
+    Bc = np.zeros((K * na, K))
     members = [[] for _ in range(na)]
     for I in range(nb):
         if agg[I] >= 0:
@@ -187,14 +189,14 @@ def tentative(agg, B, b):
         mem = members[a]
         Bs = np.concatenate([B[b * I:b * I + b] for I in mem], axis=0)
         Q, R = mgs_qr(Bs)
-        Bc[3 * a:3 * a + 3] = R
+        Bc[K * a:K * a + K] = R
         for t, I in enumerate(mem):
             for r in range(b):
-                for k in range(3):
+                for k in range(K):
                     rows.append(b * I + r)
-                    cols.append(3 * a + k)
+                    cols.append(K * a + k)
                     vals.append(Q[t * b + r, k])
-    Pt = sp.csr_matrix((vals, (rows, cols)), shape=(b * nb, 3 * na))
+    Pt = sp.csr_matrix((vals, (rows, cols)), shape=(b * nb, K * na))
     return Pt, Bc, na
 
 
@@ -225,26 +227,36 @@ def lambda_max(A, Dinv, seed, level, iters):
     return lam
 
 
-def level0_nullspace(n, L):
+def level0_nullspace(n, L, v=None):
+    """Rigid-body modes (1,0), (0,1), (-(y - L/2), x - L/2)/L per node; with v given (reading
+    G30) a fourth column: the linearisation point's velocity v_l itself."""
     i = np.arange(n + 1, dtype=np.float64) * (L / n)
     X, Y = np.meshgrid(i, i, indexing="xy")
     X, Y = X.ravel(), Y.ravel()
     Nn = X.size
-    B = np.zeros((2 * Nn, 3))
+    B = np.zeros((2 * Nn, 3 if v is None else 4))
     B[0::2, 0] = 1.0
     B[1::2, 1] = 1.0
     B[0::2, 2] = -(Y - 0.5 * L) / L
     B[1::2, 2] = (X - 0.5 * L) / L
+    if v is not None:
+        B[:, 3] = v
     return B
 
 
 def setup(J, pb=None, theta=0.04, coarse_max_dof=400, max_levels=25, power_iters=20, seed=0,
-          cheb_degree=3, cheb_lower=0.03, cheb_upper=1.1, n=None, L=512e3, agg_dist0=2, agg_dist=2):
+          cheb_degree=3, cheb_lower=0.03, cheb_upper=1.1, n=None, L=512e3, agg_dist0=2, agg_dist=2,
+          v=None, nullspace_dim=3):
+    """nullspace_dim = 4 (reading G30) appends the linearisation point v (required then) to
+    the three rigid-body modes; coarse levels then carry 4 x 4 blocks."""
     if pb is not None:
         n, L = pb.n, pb.L
     A = J.tocsr()
     b = 2
-    B = level0_nullspace(n, L)
+    if nullspace_dim == 4 and v is None:
+        raise ValueError("nullspace_dim = 4 needs the linearisation point v")
+    B = level0_nullspace(n, L, v if nullspace_dim == 4 else None)
+    K = B.shape[1]
     levels = []
     for lvl in range(max_levels):
         Dinv, blocks = block_diag_inv(A, b)
@@ -269,7 +281,7 @@ def setup(J, pb=None, theta=0.04, coarse_max_dof=400, max_levels=25, power_iters
         if fix.any():
             Ac = (Ac + sp.diags(fix.astype(np.float64))).tocsr()
         lev.update({"P": P, "R": R, "Ptent": Pt, "agg": agg, "roots": roots, "mis_rounds": rounds, "na": na})
-        A, B, b = Ac, Bc, 3
+        A, B, b = Ac, Bc, K
     coarse = levels[-1]
     coarse["chol"] = sla.cho_factor(coarse["A"].toarray(), lower=True)
     nnz0 = levels[0]["A"].nnz

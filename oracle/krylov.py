@@ -86,30 +86,40 @@ def fgmres(Aop, b, Mop=None, restart=30, rtol=1e-8, maxit=300):
 
 
 def pcg(Aop, b, Mop=None, rtol=1e-8, maxit=5000):
-    """Preconditioned conjugate gradients (textbook)."""
+    """Preconditioned conjugate gradients (textbook), x0 = 0; stop when the recursively updated
+    residual meets ||r|| <= rtol ||b||.  As for fgmres, convergence is declared only when the
+    explicit residual ||b - A x|| also meets it; otherwise CG restarts from that residual."""
     Mop = Mop or (lambda r: r.copy())
     x = np.zeros_like(b)
-    r = b.copy()
-    z = Mop(r)
-    p = z.copy()
-    rz = float(r @ z)
     bn = float(np.linalg.norm(b))
     its = 0
     if bn == 0.0:
-        return x, {"iters": 0, "converged": True}
-    while its < maxit:
-        Ap = Aop(p)
-        a = rz / float(p @ Ap)
-        x += a * p
-        r -= a * Ap
-        its += 1
-        if np.linalg.norm(r) <= rtol * bn:
-            return x, {"iters": its, "converged": True}
+        return x, {"iters": 0, "converged": True, "restarts": 0}
+    r = b.copy()
+    restarts = 0
+    while True:
         z = Mop(r)
-        rz_new = float(r @ z)
-        p = z + (rz_new / rz) * p
-        rz = rz_new
-    return x, {"iters": its, "converged": False}
+        p = z.copy()
+        rz = float(r @ z)
+        while its < maxit:
+            Ap = Aop(p)
+            a = rz / float(p @ Ap)
+            x += a * p
+            r -= a * Ap
+            its += 1
+            if np.linalg.norm(r) <= rtol * bn:
+                break
+            z = Mop(r)
+            rz_new = float(r @ z)
+            p = z + (rz_new / rz) * p
+            rz = rz_new
+        r = b - Aop(x)
+        rn = float(np.linalg.norm(r))
+        if rn <= rtol * bn:
+            return x, {"iters": its, "converged": True, "restarts": restarts, "relres_true": rn / bn}
+        if its >= maxit:
+            return x, {"iters": its, "converged": False, "restarts": restarts, "relres_true": rn / bn}
+        restarts += 1
 
 
 def jacobi(J):

@@ -73,11 +73,16 @@ def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
             kst = {"iters": 0}
         elif linsolve == "jacobi_fgmres":
             vt, kst = krylov.fgmres(lambda x: J @ x, R, krylov.jacobi(J), restart, krtol, krylov_maxit)
-        elif linsolve == "amg_fgmres":
+        elif linsolve in ("amg_fgmres", "amg_pcg"):
             from . import amg
-            H = amg.setup(J, pb, **(amg_params or {}))
-            vt, kst = krylov.fgmres(lambda x: J @ x, R, lambda r: amg.vcycle(H, r), restart,
-                                    krtol, krylov_maxit)
+            # the linearisation point v is the fourth near-nullspace column when
+            # amg_params["nullspace_dim"] == 4 (reading G30); ignored otherwise
+            H = amg.setup(J, pb, v=v, **(amg_params or {}))
+            if linsolve == "amg_fgmres":
+                vt, kst = krylov.fgmres(lambda x: J @ x, R, lambda r: amg.vcycle(H, r), restart,
+                                        krtol, krylov_maxit)
+            else:
+                vt, kst = krylov.pcg(lambda x: J @ x, R, lambda r: amg.vcycle(H, r), krtol, krylov_maxit)
             kst["levels"] = len(H["levels"])
         else:
             raise ValueError(linsolve)

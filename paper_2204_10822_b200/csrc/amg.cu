@@ -138,6 +138,28 @@ __device__ __forceinline__ bool invert_block(const double* a, double* o) {
     const double id = 1.0 / det;
     o[0] = a[3] * id; o[1] = -a[1] * id; o[2] = -a[2] * id; o[3] = a[0] * id;
     return true;
+  } else if (B == 4) {
+    // Gauss-Jordan without pivoting: diagonal blocks of the Galerkin operators are SPD
+    // (dropped near-nullspace columns get a unit diagonal, k_fix_zero_diag)
+    double m[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) { m[t] = a[t]; o[t] = (t % 5 == 0) ? 1.0 : 0.0; }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double p = m[k * 4 + k];
+      if (p == 0.0) return false;
+      const double ip = 1.0 / p;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { m[k * 4 + j] *= ip; o[k * 4 + j] *= ip; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i == k) continue;
+        const double f = m[i * 4 + k];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { m[i * 4 + j] -= f * m[k * 4 + j]; o[i * 4 + j] -= f * o[k * 4 + j]; }
+      }
+    }
+    return true;
   } else {
     const double c00 = a[4] * a[8] - a[5] * a[7];
     const double c01 = a[5] * a[6] - a[3] * a[8];
@@ -377,29 +399,31 @@ __global__ void k_seg_starts(int na, int nb, const int* __restrict__ skey, int* 
   start[a] = lo;
 }
 
-// per aggregate: two-pass MGS of the stacked near-nullspace rows (B x 3 per member)
-template <int B>
+// per aggregate: two-pass MGS of the stacked near-nullspace rows (B x K per member)
+template <int B, int K>
 __global__ void k_tentative(int na, const int* __restrict__ start, const int* __restrict__ members,
                             const double* __restrict__ Bn, const int* __restrict__ prp, double* __restrict__ pval,
                             double* __restrict__ Bc) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= na) return;
   const int m0 = start[a], m1 = start[a + 1];
-  double R[9];
+  double R[K * K];
 #pragma unroll
-  for (int t = 0; t < 9; ++t) R[t] = 0.0;
-  bool keep[3] = {false, false, false};
+  for (int t = 0; t < K * K; ++t) R[t] = 0.0;
+  bool keep[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) keep[k] = false;
   // Q is written directly into P_tent's blocks (one block per member, column agg a)
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < K; ++k) {
     // v = B[:,k]
     double n0 = 0.0;
     for (int t = m0; t < m1; ++t) {
       const int I = members[t];
-      double* q = pval + (long long)prp[I] * B * 3;
+      double* q = pval + (long long)prp[I] * B * K;
 #pragma unroll
       for (int rr = 0; rr < B; ++rr) {
-        const double v = Bn[((long long)I * B + rr) * 3 + k];
-        q[rr * 3 + k] = v;
+        const double v = Bn[((long long)I * B + rr) * K + k];
+        q[rr * K + k] = v;
         n0 += v * v;
       }
     }
@@ -409,36 +433,36 @@ __global__ void k_tentative(int na, const int* __restrict__ start, const int* __
         if (!keep[j]) continue;
         double rj = 0.0;
         for (int t = m0; t < m1; ++t) {
-          const double* q = pval + (long long)prp[members[t]] * B * 3;
+          const double* q = pval + (long long)prp[members[t]] * B * K;
 #pragma unroll
-          for (int rr = 0; rr < B; ++rr) rj += q[rr * 3 + j] * q[rr * 3 + k];
+          for (int rr = 0; rr < B; ++rr) rj += q[rr * K + j] * q[rr * K + k];
         }
-        R[j * 3 + k] += rj;
+        R[j * K + k] += rj;
         for (int t = m0; t < m1; ++t) {
-          double* q = pval + (long long)prp[members[t]] * B * 3;
+          double* q = pval + (long long)prp[members[t]] * B * K;
 #pragma unroll
-          for (int rr = 0; rr < B; ++rr) q[rr * 3 + k] -= rj * q[rr * 3 + j];
+          for (int rr = 0; rr < B; ++rr) q[rr * K + k] -= rj * q[rr * K + j];
         }
       }
     }
     double nv = 0.0;
     for (int t = m0; t < m1; ++t) {
-      const double* q = pval + (long long)prp[members[t]] * B * 3;
+      const double* q = pval + (long long)prp[members[t]] * B * K;
 #pragma unroll
-      for (int rr = 0; rr < B; ++rr) nv += q[rr * 3 + k] * q[rr * 3 + k];
+      for (int rr = 0; rr < B; ++rr) nv += q[rr * K + k] * q[rr * K + k];
     }
     nv = sqrt(nv);
     keep[k] = (nv > 1e-8 * n0) && (nv > 0.0);
     const double sc = keep[k] ? 1.0 / nv : 0.0;
-    if (keep[k]) R[k * 3 + k] = nv;
+    if (keep[k]) R[k * K + k] = nv;
     for (int t = m0; t < m1; ++t) {
-      double* q = pval + (long long)prp[members[t]] * B * 3;
+      double* q = pval + (long long)prp[members[t]] * B * K;
 #pragma unroll
-      for (int rr = 0; rr < B; ++rr) q[rr * 3 + k] *= sc;
+      for (int rr = 0; rr < B; ++rr) q[rr * K + k] *= sc;
     }
   }
 #pragma unroll
-  for (int t = 0; t < 9; ++t) Bc[(long long)a * 9 + t] = R[t];
+  for (int t = 0; t < K * K; ++t) Bc[(long long)a * K * K + t] = R[t];
 }
 
 __global__ void k_flag_agg(int nb, const int* __restrict__ agg, int* __restrict__ f) {
@@ -1002,7 +1026,7 @@ static void transpose(Ctx& c, const BsrMat& X, DBuf<int>& trp, DBuf<int>& tci, D
 }
 
 // ------------------------------------------------------------------ prolongator smoothing
-template <int B>
+template <int B, int K>
 __global__ void k_smooth_p(int nb, const int* __restrict__ trp, const int* __restrict__ tci,
                            const double* __restrict__ tval, const double* __restrict__ dinv,
                            const int* __restrict__ agg, const int* __restrict__ prp_t, const double* __restrict__ pt_val,
@@ -1012,22 +1036,23 @@ __global__ void k_smooth_p(int nb, const int* __restrict__ trp, const int* __res
   const double* D = dinv + (long long)r * B * B;
   const int ar = agg[r];
   for (int e = trp[r]; e < trp[r + 1]; ++e) {
-    const double* T = tval + (long long)e * B * 3;
-    double* Pv = pval + (long long)e * B * 3;
+    const double* T = tval + (long long)e * B * K;
+    double* Pv = pval + (long long)e * B * K;
 #pragma unroll
     for (int a = 0; a < B; ++a)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
+      for (int k = 0; k < K; ++k) {
         double s = 0.0;
 #pragma unroll
-        for (int b = 0; b < B; ++b) s += D[a * B + b] * T[b * 3 + k];
+        for (int b = 0; b < B; ++b) s += D[a * B + b] * T[b * K + k];
         double v = -omega * s;
-        if (tci[e] == ar) v += pt_val[(long long)prp_t[r] * B * 3 + a * 3 + k];
-        Pv[a * 3 + k] = v;
+        if (tci[e] == ar) v += pt_val[(long long)prp_t[r] * B * K + a * K + k];
+        Pv[a * K + k] = v;
       }
   }
 }
 
+template <int K>
 __global__ void k_fix_zero_diag(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
                                 double* __restrict__ val) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1035,8 +1060,8 @@ __global__ void k_fix_zero_diag(int nb, const int* __restrict__ rp, const int* _
   for (int e = rp[r]; e < rp[r + 1]; ++e)
     if (ci[e] == r) {
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        if (val[(long long)e * 9 + k * 4] == 0.0) val[(long long)e * 9 + k * 4] = 1.0;
+      for (int k = 0; k < K; ++k)
+        if (val[(long long)e * K * K + k * (K + 1)] == 0.0) val[(long long)e * K * K + k * (K + 1)] = 1.0;
     }
 }
 
@@ -1392,6 +1417,9 @@ __device__ __forceinline__ void load_xblk(const double* __restrict__ x, int col,
     const double* p = x + (long long)col * 4;
     double w;
     asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(xv[0]), "=d"(xv[1]), "=d"(xv[2]), "=d"(w) : "l"(p));
+  } else if constexpr (BC == 4) {
+    const double* p = x + (long long)col * 4;
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(xv[0]), "=d"(xv[1]), "=d"(xv[2]), "=d"(xv[3]) : "l"(p));
   } else {
     const double2 v = __ldg(reinterpret_cast<const double2*>(x) + col);
     xv[0] = v.x;
@@ -1548,6 +1576,151 @@ __global__ void __launch_bounds__(256) k_gresid(int nb, const int* __restrict__ 
   }
 }
 
+// ------------------------------------------------------------------ row-component kernels (b = 4)
+// With nullspace_dim = 4 (reading G30) coarse blocks are 4 x 4 = 128 B, i.e. one block row of
+// a block is 32 B: BR consecutive lanes read the BR rows of ONE block (row-major block storage,
+// Level::val / Pval / Rval as the SpGEMM writes them) with a single 32-B (BC = 4) or 16-B
+// (BC = 2) load each, and the block's x entries with one 32-B / 16-B load (same address for
+// the BR lanes: one transaction).  A group of G = BR * S lanes owns one block row and keeps
+// S blocks in flight; lane l accumulates row component a = l % BR over slot l / BR's blocks,
+// then the S partial sums of component a are combined by an xor-butterfly (fixed order).
+template <int BC>
+__device__ __forceinline__ void load_row(const double* __restrict__ p, double v[BC]) {
+  if constexpr (BC == 4) {
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+  } else {
+    const double2 w = __ldg(reinterpret_cast<const double2*>(p));
+    v[0] = w.x;
+    v[1] = w.y;
+  }
+}
+
+template <int BR, int BC, int S>
+__device__ __forceinline__ double grpA_row(int row, int nb, int lig, const int* __restrict__ rp,
+                                           const int* __restrict__ ci, const double* __restrict__ val,
+                                           const double* __restrict__ x) {
+  constexpr int G = BR * S;
+  const int a = lig % BR, slot = lig / BR;
+  double acc = 0.0;
+  if (row < nb) {
+    const int e1 = __ldg(rp + row + 1);
+    int e = __ldg(rp + row) + slot;
+    for (; e + S < e1; e += 2 * S) {
+      const int c0 = __ldg(ci + e), c1 = __ldg(ci + e + S);
+      double v0[BC], v1[BC], x0[BC], x1[BC];
+      load_row<BC>(val + ((long long)e * BR + a) * BC, v0);
+      load_row<BC>(val + ((long long)(e + S) * BR + a) * BC, v1);
+      load_xblk<BC>(x, c0, x0);
+      load_xblk<BC>(x, c1, x1);
+#pragma unroll
+      for (int b = 0; b < BC; ++b) acc += v0[b] * x0[b];
+#pragma unroll
+      for (int b = 0; b < BC; ++b) acc += v1[b] * x1[b];
+    }
+    for (; e < e1; e += S) {
+      double v0[BC], x0[BC];
+      load_row<BC>(val + ((long long)e * BR + a) * BC, v0);
+      load_xblk<BC>(x, __ldg(ci + e), x0);
+#pragma unroll
+      for (int b = 0; b < BC; ++b) acc += v0[b] * x0[b];
+    }
+  }
+#pragma unroll
+  for (int off = BR; off < G; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
+  return acc;
+}
+
+// y = yin + A x (yin may be NULL; yin == y: in place), row-major BR x BC blocks
+template <int BR, int BC, int S>
+__global__ void __launch_bounds__(256) k_aspmv(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                                               const double* __restrict__ val, const double* __restrict__ x,
+                                               const double* yin, double* y) {
+  constexpr int G = BR * S, SR = vstride(BR);
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int row = (int)(t / G), lig = (int)(t % G);
+  const bool own = row < nb && lig < BR;
+  const long long i = (long long)row * SR + lig;
+  const double y0 = (own && yin) ? yin[i] : 0.0;
+  const double acc = grpA_row<BR, BC, S>(row, nb, lig, rp, ci, val, x);
+  if (own) y[i] = y0 + acc;
+}
+
+// Chebyshev step on a b = 4 level (semantics of k_gcheb)
+template <int S>
+__global__ void __launch_bounds__(256) k_acheb4(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                const double* __restrict__ val, const double* __restrict__ dinv,
+                                                const double* __restrict__ d, double* __restrict__ r,
+                                                double* __restrict__ x, double* __restrict__ dout, double c1,
+                                                double c2, int first, int want_r, int want_d) {
+  constexpr int G = 4 * S;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int row = (int)(t / G), lig = (int)(t % G);
+  const bool own = row < nb && lig < 4;
+  const long long i = (long long)row * 4 + lig;
+  double dv = 0.0, xv = 0.0, rv = 0.0, D[4] = {0.0, 0.0, 0.0, 0.0};
+  if (own) {
+    dv = d[i];
+    if (!first) xv = x[i];
+    if (want_r) rv = r[i];
+    if (want_d) load_row<4>(dinv + (long long)row * 16 + lig * 4, D);
+  }
+  double acc = 0.0;
+  if (want_r) acc = grpA_row<4, 4, S>(row, nb, lig, rp, ci, val, d);
+  if (own) x[i] = xv + dv;
+  if (!want_r) return;  // uniform across the launch
+  rv -= acc;
+  if (own) r[i] = rv;
+  if (!want_d) return;
+  double z = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) z += D[k] * __shfl_sync(0xffffffffu, rv, k, G);
+  if (own) dout[i] = c1 * dv + c2 * z;
+}
+
+// r = b - A x (x may be NULL: r = b); d = c2 Dinv r on a b = 4 level
+template <int S>
+__global__ void __launch_bounds__(256) k_aresid4(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                 const double* __restrict__ val, const double* __restrict__ dinv,
+                                                 const double* __restrict__ b, const double* __restrict__ x,
+                                                 double* __restrict__ r, double* __restrict__ d, double c2) {
+  constexpr int G = 4 * S;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int row = (int)(t / G), lig = (int)(t % G);
+  const bool own = row < nb && lig < 4;
+  const long long i = (long long)row * 4 + lig;
+  double bo = 0.0, D[4] = {0.0, 0.0, 0.0, 0.0};
+  if (own) {
+    bo = b[i];
+    load_row<4>(dinv + (long long)row * 16 + lig * 4, D);
+  }
+  const double acc = x ? grpA_row<4, 4, S>(row, nb, lig, rp, ci, val, x) : 0.0;
+  const double rv = bo - acc;
+  if (own) r[i] = rv;
+  double z = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) z += D[k] * __shfl_sync(0xffffffffu, rv, k, G);
+  if (own) d[i] = c2 * z;
+}
+
+// slots (blocks in flight per block row) for the row-component kernels
+static int pick_slots(long long nnzb, int nb, int BR) {
+  static const int shift = getenv("SEAICE_SLOT_SHIFT") ? atoi(getenv("SEAICE_SLOT_SHIFT")) : 0;  // tuning aid
+  const double avg = nb > 0 ? (double)nnzb / nb : 1.0;
+  int s = avg <= 3.0 ? 1 : avg <= 6.0 ? 2 : avg <= 16.0 ? 4 : 8;
+  if ((long long)nb * 32 <= 148LL * 2048) s = 8;  // small levels: shortest dependent-load chains
+  s = shift >= 0 ? (s << shift) : (s >> -shift);
+  const int smax = 32 / BR < 8 ? 32 / BR : 8;
+  return s < 1 ? 1 : (s > smax ? smax : s);
+}
+#define SI_SDISPATCH(S_, CALL)                        \
+  switch (S_) {                                       \
+    case 1: { constexpr int SS = 1; CALL; } break;   \
+    case 2: { constexpr int SS = 2; CALL; } break;   \
+    case 4: { constexpr int SS = 4; CALL; } break;   \
+    default: { constexpr int SS = 8; CALL; } break;  \
+  }
+static int agrid(int nb, int G) { return (int)(((long long)nb * G + 255) / 256); }
+
 static int pick_group(long long nnzb, int nb) {
   static const int shift = getenv("SEAICE_GROUP_SHIFT") ? atoi(getenv("SEAICE_GROUP_SHIFT")) : 0;  // tuning aid
   const double avg = nb > 0 ? (double)nnzb / nb : 1.0;
@@ -1582,6 +1755,16 @@ static void gspmv(Ctx& c, int nb, int br, int bc, long long nnzb, const int* rp,
     else SI_GDISPATCH(G, (k_gspmv<2, 3, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
   } else if (br == 3 && bc == 2) {
     SI_GDISPATCH(G, (k_gspmv<3, 2, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
+  } else if (br == 4 || bc == 4) {
+    // b = 4 hierarchies (reading G30): row-major blocks, row-component lanes (val is AoS here)
+    const int Sl = pick_slots(nnzb, nb, br);
+    if (br == 4 && bc == 4) {
+      SI_SDISPATCH(Sl, (k_aspmv<4, 4, SS><<<agrid(nb, 4 * SS), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
+    } else if (br == 2) {
+      SI_SDISPATCH(Sl, (k_aspmv<2, 4, SS><<<agrid(nb, 2 * SS), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
+    } else {
+      SI_SDISPATCH(Sl, (k_aspmv<4, 2, SS><<<agrid(nb, 4 * SS), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
+    }
   } else {
     SI_GDISPATCH(G, (k_gspmv<2, 2, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
   }
@@ -1613,7 +1796,7 @@ static double power_lambda(Ctx& c, Level& L, int lvl) {
     if (lvl == 0 && B == 2)
       stencil_spmv(c, x, y);  // the finest operator is the stencil itself
     else
-      gspmv(c, L.nb, B, B, L.nnzb, L.rp.get(), L.ci.get(), L.valT.get(), x, nullptr, y);
+      gspmv(c, L.nb, B, B, L.nnzb, L.rp.get(), L.ci.get(), B == 4 ? L.val.get() : L.valT.get(), x, nullptr, y);
     k_dinv_apply<B><<<grid_for(L.nb), kThreads, 0, c.s>>>(L.nb, L.dinv.get(), y);
     k_sqnorm_part<<<g, kThreads, 0, c.s>>>(N, y, part);
     k_sum_to<<<1, 1024, 0, c.s>>>(part, g, ny2);
@@ -1689,7 +1872,7 @@ static int aggregate_level(Ctx& c, Level& L, int lvl, const double* dnorm, Scrat
   return na;
 }
 
-template <int B>
+template <int B, int K>
 static void build_transfer(Ctx& c, Level& L, Level& Lc, int lvl, int na, Scratch& S) {
   const int nb = L.nb;
   // members sorted by aggregate (stable: node order inside an aggregate)
@@ -1721,53 +1904,53 @@ static void build_transfer(Ctx& c, Level& L, Level& Lc, int lvl, int na, Scratch
   exclusive_scan(c, f, ptrp, nb + 1);
   const int ptn = read_scalar(c, ptrp + nb);
   int* ptci = S.get<int>(ptn);
-  double* ptval = S.get<double>((size_t)ptn * B * 3);
+  double* ptval = S.get<double>((size_t)ptn * B * K);
   k_ptent_ci<<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.agg.get(), ptrp, ptci);
   SI_LAUNCHED(c);
-  Lc.B.ensure(c.al, (size_t)na * 9);
-  k_tentative<B><<<grid_for(na, 128), 128, 0, c.s>>>(na, start, members, L.B.get(), ptrp, ptval, Lc.B.get());
+  Lc.B.ensure(c.al, (size_t)na * K * K);
+  k_tentative<B, K><<<grid_for(na, 128), 128, 0, c.s>>>(na, start, members, L.B.get(), ptrp, ptval, Lc.B.get());
   SI_LAUNCHED(c);
   tick(c, "tentative", lvl);
-  BsrMat Pt{nb, na, B, 3, ptn, ptrp, ptci, ptval};
+  BsrMat Pt{nb, na, B, K, ptn, ptrp, ptci, ptval};
   // T = A P_tent ; P = P_tent - omega Dinv T  (P takes T's pattern)
   long long tn = 0;
-  spgemm<B, B, 3>(c, view(L), Pt, L.Prp, L.Pci, L.Tval, tn);
+  spgemm<B, B, K>(c, view(L), Pt, L.Prp, L.Pci, L.Tval, tn);
   tick(c, "A*Pt", lvl);
   L.Pnnzb = tn;
-  L.Pval.ensure(c.al, (size_t)tn * B * 3);
+  L.Pval.ensure(c.al, (size_t)tn * B * K);
   const double omega = 4.0 / (3.0 * L.lmax);
-  k_smooth_p<B><<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.Prp.get(), L.Pci.get(), L.Tval.get(), L.dinv.get(),
+  k_smooth_p<B, K><<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.Prp.get(), L.Pci.get(), L.Tval.get(), L.dinv.get(),
                                                     L.agg.get(), ptrp, ptval, omega, L.Pval.get());
   SI_LAUNCHED(c);
   L.nbc = na;
-  BsrMat P{nb, na, B, 3, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.Pval.get()};
+  BsrMat P{nb, na, B, K, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.Pval.get()};
   tick(c, "smoothP", lvl);
   // R = P^T
-  transpose<B, 3>(c, P, L.Rrp, L.Rci, L.Rval);
+  transpose<B, K>(c, P, L.Rrp, L.Rci, L.Rval);
   L.Rnnzb = L.Pnnzb;
   tick(c, "transpose", lvl);
-  BsrMat R{na, nb, 3, B, L.Rnnzb, L.Rrp.get(), L.Rci.get(), L.Rval.get()};
+  BsrMat R{na, nb, K, B, L.Rnnzb, L.Rrp.get(), L.Rci.get(), L.Rval.get()};
   if (B == 2) {
     // finest level: A_c = (R A) P — the R A intermediate has one row per aggregate instead of
     // A P's one row per fine node and the product count halves (measured 37 -> 27 ms at n = 2048)
     long long ran = 0;
-    spgemm<3, B, B>(c, R, view(L), c.ap_rp, c.ap_ci, c.ap_val, ran);
+    spgemm<K, B, B>(c, R, view(L), c.ap_rp, c.ap_ci, c.ap_val, ran);
     tick(c, "R*A", lvl);
-    BsrMat RA{na, nb, 3, B, ran, c.ap_rp.get(), c.ap_ci.get(), c.ap_val.get()};
-    spgemm<3, B, 3>(c, RA, P, Lc.rp, Lc.ci, Lc.val, Lc.nnzb);
+    BsrMat RA{na, nb, K, B, ran, c.ap_rp.get(), c.ap_ci.get(), c.ap_val.get()};
+    spgemm<K, B, K>(c, RA, P, Lc.rp, Lc.ci, Lc.val, Lc.nnzb);
     tick(c, "RA*P", lvl);
   } else {
     // coarse levels (wide rows): A_c = R (A P) measured faster
     long long apn = 0;
-    spgemm<B, B, 3>(c, view(L), P, c.ap_rp, c.ap_ci, c.ap_val, apn);
+    spgemm<B, B, K>(c, view(L), P, c.ap_rp, c.ap_ci, c.ap_val, apn);
     tick(c, "A*P", lvl);
-    BsrMat AP{nb, na, B, 3, apn, c.ap_rp.get(), c.ap_ci.get(), c.ap_val.get()};
-    spgemm<3, B, 3>(c, R, AP, Lc.rp, Lc.ci, Lc.val, Lc.nnzb);
+    BsrMat AP{nb, na, B, K, apn, c.ap_rp.get(), c.ap_ci.get(), c.ap_val.get()};
+    spgemm<K, B, K>(c, R, AP, Lc.rp, Lc.ci, Lc.val, Lc.nnzb);
     tick(c, "R*AP", lvl);
   }
   Lc.nb = na;
-  Lc.b = 3;
-  k_fix_zero_diag<<<grid_for(na), kThreads, 0, c.s>>>(na, Lc.rp.get(), Lc.ci.get(), Lc.val.get());
+  Lc.b = K;
+  k_fix_zero_diag<K><<<grid_for(na), kThreads, 0, c.s>>>(na, Lc.rp.get(), Lc.ci.get(), Lc.val.get());
   SI_LAUNCHED(c);
 }
 
@@ -1810,15 +1993,20 @@ void amg_free(Ctx& c) {
   c.amg_ready = false;
 }
 
-__global__ void k_level0_nullspace(int n, double L, double* __restrict__ B) {
+// rigid-body modes per node [2][K]; K = 4 appends the linearisation point v (reading G30)
+__global__ void k_level0_nullspace(int n, double L, int K, const double* __restrict__ v, double* __restrict__ B) {
   const int node = blockIdx.x * blockDim.x + threadIdx.x;
   const int s = n + 1;
   if (node >= s * s) return;
   const double dx = L / n;
   const double x = (node % s) * dx, y = (node / s) * dx;
-  double* b = B + (long long)node * 6;
+  double* b = B + (long long)node * 2 * K;
   b[0] = 1.0; b[1] = 0.0; b[2] = -(y - 0.5 * L) / L;
-  b[3] = 0.0; b[4] = 1.0; b[5] = (x - 0.5 * L) / L;
+  b[K] = 0.0; b[K + 1] = 1.0; b[K + 2] = (x - 0.5 * L) / L;
+  if (K == 4) {
+    b[3] = v[2 * node];
+    b[7] = v[2 * node + 1];
+  }
 }
 
 void vgraph_destroy(Ctx& c);
@@ -1840,8 +2028,10 @@ void amg_setup_impl(Ctx& c) {
   L0.val.ensure(c.al, (size_t)L0.nnzb * 4);
   k_stencil_to_bsr<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L0.rp.get(), L0.val.get());
   SI_LAUNCHED(c);
-  L0.B.ensure(c.al, (size_t)c.Nn * 6);
-  k_level0_nullspace<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.p.L, L0.B.get());
+  const int K = c.p.nullspace_dim;
+  SI_CHECK(K == 3 || c.lin_v.get(), SEAICE_ESTATE, "nullspace_dim = 4 needs an assembled linearisation point");
+  L0.B.ensure(c.al, (size_t)c.Nn * 2 * K);
+  k_level0_nullspace<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.p.L, K, c.lin_v.get(), L0.B.get());
   SI_LAUNCHED(c);
   tick(c, "to_bsr", 0);
   long long nnz_total = 0;
@@ -1852,10 +2042,12 @@ void amg_setup_impl(Ctx& c) {
     double* dnorm = S.get<double>(L.nb);
     tick(c, nullptr, lvl);
     if (L.b == 2) level_diag<2>(c, L, S, dnorm);
-    else level_diag<3>(c, L, S, dnorm);
+    else if (L.b == 3) level_diag<3>(c, L, S, dnorm);
+    else level_diag<4>(c, L, S, dnorm);
     tick(c, "diag", lvl);
-    if (lvl > 0) tile_copy(c, L.valT, L.val.get(), L.nnzb, L.b * L.b);
-    L.lmax = (L.b == 2) ? power_lambda<2>(c, L, lvl) : power_lambda<3>(c, L, lvl);
+    if (lvl > 0 && L.b != 4) tile_copy(c, L.valT, L.val.get(), L.nnzb, L.b * L.b);
+    L.lmax = (L.b == 2) ? power_lambda<2>(c, L, lvl) : (L.b == 3) ? power_lambda<3>(c, L, lvl)
+                                                                  : power_lambda<4>(c, L, lvl);
     tick(c, "power", lvl);
     nnz_total += L.nnzb * L.b * L.b;
     const long long ndof = (long long)L.nb * L.b;
@@ -1867,18 +2059,27 @@ void amg_setup_impl(Ctx& c) {
     }
     const bool last_allowed = (lvl + 1 >= c.p.max_levels);
     if (ndof <= c.p.coarse_max_dof || last_allowed) break;
-    const int na = (L.b == 2) ? aggregate_level<2>(c, L, lvl, dnorm, S) : aggregate_level<3>(c, L, lvl, dnorm, S);
+    const int na = (L.b == 2)   ? aggregate_level<2>(c, L, lvl, dnorm, S)
+                   : (L.b == 3) ? aggregate_level<3>(c, L, lvl, dnorm, S)
+                                : aggregate_level<4>(c, L, lvl, dnorm, S);
     tick(c, "aggregate", lvl);
     if (na == 0 || na > 0.9 * L.nb) break;
     if ((int)c.lv.size() == c.nlev) c.lv.emplace_back();  // may move Level objects (DBufs are handles)
     Level& Lc = c.lv[c.nlev];
     Level& Lf = c.lv[lvl];
     ++c.nlev;
-    if (Lf.b == 2) build_transfer<2>(c, Lf, Lc, lvl, na, S);
-    else build_transfer<3>(c, Lf, Lc, lvl, na, S);
+    if (K == 3) {
+      if (Lf.b == 2) build_transfer<2, 3>(c, Lf, Lc, lvl, na, S);
+      else build_transfer<3, 3>(c, Lf, Lc, lvl, na, S);
+    } else {
+      if (Lf.b == 2) build_transfer<2, 4>(c, Lf, Lc, lvl, na, S);
+      else build_transfer<4, 4>(c, Lf, Lc, lvl, na, S);
+    }
     tick(c, nullptr, lvl);
-    tile_copy(c, Lf.PvalT, Lf.Pval.get(), Lf.Pnnzb, Lf.b * 3);
-    tile_copy(c, Lf.RvalT, Lf.Rval.get(), Lf.Rnnzb, 3 * Lf.b);
+    if (K != 4) {  // b = 4 kernels read the row-major blocks directly
+      tile_copy(c, Lf.PvalT, Lf.Pval.get(), Lf.Pnnzb, Lf.b * K);
+      tile_copy(c, Lf.RvalT, Lf.Rval.get(), Lf.Rnnzb, K * Lf.b);
+    }
     tick(c, "tile_PR", lvl);
   }
   Level& Lc = c.lv[c.nlev - 1];
@@ -1937,9 +2138,16 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
                                                             (double2*)r, (double2*)d, 1.0 / k.th);
     } else {
       const int G = pick_group(L.nnzb, L.nb);
-      SI_GDISPATCH(G, (k_gresid<3, GG><<<ggrid(L.nb, GG), 256, 0, c.s>>>(
-                          L.nb, L.rp.get(), L.ci.get(), L.valT.get(), L.dinv.get(), b, pre ? nullptr : x, r, d,
-                          1.0 / k.th)))
+      if (L.b == 3)
+        SI_GDISPATCH(G, (k_gresid<3, GG><<<ggrid(L.nb, GG), 256, 0, c.s>>>(
+                            L.nb, L.rp.get(), L.ci.get(), L.valT.get(), L.dinv.get(), b, pre ? nullptr : x, r, d,
+                            1.0 / k.th)))
+      else {
+        const int Sl = pick_slots(L.nnzb, L.nb, 4);
+        SI_SDISPATCH(Sl, (k_aresid4<SS><<<agrid(L.nb, 4 * SS), 256, 0, c.s>>>(
+                             L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), b, pre ? nullptr : x, r, d,
+                             1.0 / k.th)))
+      }
     }
     SI_LAUNCHED(c);
     const double B = L.b;
@@ -1984,9 +2192,16 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
                                                      want_d);
     } else {
       const int G = pick_group(L.nnzb, L.nb);
-      SI_GDISPATCH(G, (k_gcheb<3, GG><<<ggrid(L.nb, GG), 256, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.valT.get(),
-                                                                       L.dinv.get(), d, r, x, d2, c1, c2, first,
-                                                                       want_r, want_d)))
+      if (L.b == 3)
+        SI_GDISPATCH(G, (k_gcheb<3, GG><<<ggrid(L.nb, GG), 256, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.valT.get(),
+                                                                         L.dinv.get(), d, r, x, d2, c1, c2, first,
+                                                                         want_r, want_d)))
+      else {
+        const int Sl = pick_slots(L.nnzb, L.nb, 4);
+        SI_SDISPATCH(Sl, (k_acheb4<SS><<<agrid(L.nb, 4 * SS), 256, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(),
+                                                                             L.val.get(), L.dinv.get(), d, r, x, d2,
+                                                                             c1, c2, first, want_r, want_d)))
+      }
     }
     SI_LAUNCHED(c);
     {
@@ -2014,13 +2229,17 @@ static void vcycle_level(Ctx& c, int l, const double* b, double* x) {
   Level& Lc = c.lv[l + 1];
   // r_c = R r
   prof_begin(c);
-  gspmv(c, L.nbc, 3, L.b, L.Rnnzb, L.Rrp.get(), L.Rci.get(), L.RvalT.get(), L.r.get(), nullptr, Lc.rhs.get());
-  prof_end(c, PC_TRANSFER, L.Rnnzb * (24.0 * L.b + 4.0) + 4.0 * (L.nbc + 1) + 8.0 * L.b * L.nb + 24.0 * L.nbc);
+  gspmv(c, L.nbc, Lc.b, L.b, L.Rnnzb, L.Rrp.get(), L.Rci.get(), Lc.b == 4 ? L.Rval.get() : L.RvalT.get(), L.r.get(),
+        nullptr, Lc.rhs.get());
+  prof_end(c, PC_TRANSFER,
+           L.Rnnzb * (8.0 * Lc.b * L.b + 4.0) + 4.0 * (L.nbc + 1) + 8.0 * L.b * L.nb + 8.0 * Lc.b * L.nbc);
   vcycle_level(c, l + 1, Lc.rhs.get(), Lc.x.get());
   // x += P e_c
   prof_begin(c);
-  gspmv(c, L.nb, L.b, 3, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.PvalT.get(), Lc.x.get(), x, x);
-  prof_end(c, PC_TRANSFER, L.Pnnzb * (24.0 * L.b + 4.0) + 4.0 * (L.nb + 1) + 16.0 * L.b * L.nb + 24.0 * L.nbc);
+  gspmv(c, L.nb, L.b, Lc.b, L.Pnnzb, L.Prp.get(), L.Pci.get(), Lc.b == 4 ? L.Pval.get() : L.PvalT.get(), Lc.x.get(),
+        x, x);
+  prof_end(c, PC_TRANSFER,
+           L.Pnnzb * (8.0 * Lc.b * L.b + 4.0) + 4.0 * (L.nb + 1) + 16.0 * L.b * L.nb + 8.0 * Lc.b * L.nbc);
   smooth(c, l, b, x, false);
 }
 

@@ -70,6 +70,8 @@ void validate(const seaice_params* p) {
   SI_CHECK(p->cheb_degree0 >= 0 && p->cheb_degree0 <= 16, SEAICE_EINVAL, "cheb_degree0 in [0,16]");
   SI_CHECK(p->matfree == 0 || p->matfree == 1, SEAICE_EINVAL, "matfree must be 0 or 1");
   SI_CHECK(p->krylov_forcing == 0 || p->krylov_forcing == 1, SEAICE_EINVAL, "krylov_forcing must be 0 or 1");
+  SI_CHECK(p->nullspace_dim == 3 || p->nullspace_dim == 4, SEAICE_EINVAL, "nullspace_dim must be 3 or 4");
+  SI_CHECK(p->krylov_method == 0 || p->krylov_method == 1, SEAICE_EINVAL, "krylov_method must be 0 or 1");
 }
 
 int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* out) {
@@ -259,6 +261,8 @@ void seaice_default_params(seaice_params* p, int32_t n) {
   p->cheb_degree0 = 0;  // measured no gain on B200 (grid barriers ~ launch gaps in the graph)
   p->matfree = 0;       // the assembled 19-value stencil SpMV is ~4x cheaper than the matrix-free apply
   p->krylov_forcing = 0;  // fixed krylov_rtol per Newton solve (reading G13)
+  p->nullspace_dim = 3;
+  p->krylov_method = 0;
 }
 
 int seaice_create(const seaice_params* p, const seaice_runtime* rt, seaice_ctx** out) {
@@ -310,9 +314,9 @@ int seaice_destroy(seaice_ctx* h) {
   Ctx& c = h->c;
   cudaStreamSynchronize(c.s);
   amg_free(c);
-  DBuf<double>* dbs[] = {&c.P, &c.rhoh, &c.F, &c.vprev, &c.vair, &c.vocean, &c.pi, &c.vwork, &c.load, &c.Jst, &c.mf_v, &c.mf_pi,
+  DBuf<double>* dbs[] = {&c.P, &c.rhoh, &c.F, &c.vprev, &c.vair, &c.vocean, &c.pi, &c.vwork, &c.load, &c.Jst, &c.mf_v, &c.mf_pi, &c.lin_v,
                          &c.R, &c.csr_val, &c.part, &c.scal, &c.vt, &c.pit, &c.V, &c.Z, &c.w, &c.xk, &c.rk,
-                         &c.cinv, &c.dwork};
+                         &c.cinv, &c.dwork, &c.cg_p, &c.cg_q, &c.cg_s};
   for (auto* b : dbs) b->free_();
   c.flag.free_();
   c.csr_rp.free_();
@@ -408,7 +412,7 @@ int seaice_amg_level(seaice_ctx* h, int32_t level, seaice_bsr* A_out, seaice_bsr
     if (last)
       std::memset(P_out, 0, sizeof(*P_out));
     else
-      *P_out = seaice_bsr{L.nb, L.nbc, L.b, 3, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.Pval.get()};
+      *P_out = seaice_bsr{L.nb, L.nbc, L.b, c.lv[level + 1].b, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.Pval.get()};
   }
   if (agg_host && !last) {
     SI_CUDA(cudaMemcpyAsync(agg_host, L.agg.get(), sizeof(int) * L.nb, cudaMemcpyDeviceToHost, c.s));

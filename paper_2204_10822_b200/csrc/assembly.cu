@@ -1025,6 +1025,10 @@ void assemble_impl(Ctx& c, const double* v, const double* pi, bool jac, double* 
   if (jac) {
     c.assembled = true;
     c.amg_ready = false;
+    if (c.p.nullspace_dim == 4) {  // AMG near-nullspace column v_l (reading G30)
+      c.lin_v.ensure(c.al, c.N);
+      SI_CUDA(cudaMemcpyAsync(c.lin_v.get(), v, sizeof(double) * c.N, cudaMemcpyDeviceToDevice, c.s));
+    }
     if (c.p.matfree) {  // the matrix-free FGMRES operator needs the linearisation point
       c.mf_v.ensure(c.al, c.N);
       c.mf_pi.ensure(c.al, 12LL * c.Nc);

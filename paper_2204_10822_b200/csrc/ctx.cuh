@@ -25,7 +25,7 @@ struct Level {
   DBuf<int> Prp, Pci, Rrp, Rci;
   DBuf<double> Pval, Rval;
   DBuf<int> agg;              // aggregate id per block row (-1: isolated, zero P row)
-  DBuf<double> B;             // near-nullspace rows [nb*b][3]
+  DBuf<double> B;             // near-nullspace rows [nb*b][K], K = nullspace_dim
   // V-cycle work vectors (length nb*b)
   DBuf<double> x, rhs, r, d, d2, z;
   DBuf<double> Tval;          // A P_tent values (pattern of P), setup scratch kept for reuse
@@ -138,6 +138,7 @@ struct Ctx {
   // 19 values per node, slot-major SoA (layout in stencil.cuh)
   DBuf<double> Jst;
   DBuf<double> mf_v, mf_pi;  // (v, pi) of the last assembly, for the matrix-free FGMRES operator
+  DBuf<double> lin_v;        // v of the last assembly (AMG near-nullspace column, nullspace_dim = 4)
   DBuf<double> R;  // residual of the last assemble
   double last_res_norm = 0.0;
   // scalar CSR view (built on demand)
@@ -158,6 +159,7 @@ struct Ctx {
 
   // Krylov
   DBuf<double> V, Z, w, xk, rk;
+  DBuf<double> cg_p, cg_q, cg_s;  // PCG (krylov_method = 1): direction, A p, device scalars
 
   // AMG (lv is a pool: levels [0, nlev) are active; buffers are reused across setups)
   std::vector<Level> lv;

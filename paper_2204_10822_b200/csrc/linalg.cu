@@ -73,6 +73,9 @@ void bsr_apply(Ctx& c, int nb, int br, int bc, const int* rp, const int* ci, con
   else if (br == 3 && bc == 3) launch_bsr<3, 3>(c, nb, rp, ci, val, x, y);
   else if (br == 2 && bc == 3) launch_bsr<2, 3>(c, nb, rp, ci, val, x, y);
   else if (br == 3 && bc == 2) launch_bsr<3, 2>(c, nb, rp, ci, val, x, y);
+  else if (br == 4 && bc == 4) launch_bsr<4, 4>(c, nb, rp, ci, val, x, y);
+  else if (br == 2 && bc == 4) launch_bsr<2, 4>(c, nb, rp, ci, val, x, y);
+  else if (br == 4 && bc == 2) launch_bsr<4, 2>(c, nb, rp, ci, val, x, y);
   else throw Error(SEAICE_EINVAL, "bsr_apply: unsupported block shape");
 }
 

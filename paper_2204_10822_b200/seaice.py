@@ -36,7 +36,7 @@ class Params(C.Structure):
                 ("project_pi", C.c_int32), ("amg_seed", C.c_uint64), ("agg_dist0", C.c_int32),
                 ("agg_dist", C.c_int32), ("cheb_fused", C.c_int32),
                 ("cheb_degree0", C.c_int32), ("matfree", C.c_int32),
-                ("krylov_forcing", C.c_int32)]
+                ("krylov_forcing", C.c_int32), ("nullspace_dim", C.c_int32), ("krylov_method", C.c_int32)]
 
 
 ALLOC_T = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)

@@ -48,17 +48,20 @@ def newton_state(n, seed, iters):
     return inp, pb, v, pi
 
 
+@pytest.mark.parametrize("nsd", [3, 4])
 @pytest.mark.parametrize("n,it", [(32, 0), (32, 6), (64, 3)])
-def test_hierarchy_matches_oracle(n, it):
+def test_hierarchy_matches_oracle(n, it, nsd):
     inp, pb, v, pi = newton_state(n, n, it)
     J = pb.jacobian(v, pi, "sv")
-    H = OA.setup(J, pb)
-    ctx = make_ctx(n)
+    H = OA.setup(J, pb, v=v, nullspace_dim=nsd)
+    ctx = make_ctx(n, nullspace_dim=nsd)
     ctx.set_inputs(inp)
     ctx.assemble_jacobian(v, pi.ravel(), want_csr=False)
     nlev, oc = ctx.amg_setup()
     assert nlev == len(H["levels"])
-    assert abs(oc - H["op_complexity"]) <= 0.02 * H["op_complexity"]  # explicit zeros differ slightly
+    if nsd == 3:  # explicit zeros differ slightly; with 4 columns dropped (v = 0) columns leave
+        # zero blocks the GPU stores and scipy drops, so only the level operators are compared
+        assert abs(oc - H["op_complexity"]) <= 0.02 * H["op_complexity"]
     for l in range(nlev):
         A, P, agg = ctx.amg_level(l)
         Ao = H["levels"][l]["A"]
@@ -93,12 +96,13 @@ def test_galerkin_and_transfer_properties():
         assert len(np.unique(agg[agg >= 0])) == P["nbcols"]        # every aggregate non-empty
 
 
-def test_vcycle_parity_and_symmetry():
+@pytest.mark.parametrize("nsd", [3, 4])
+def test_vcycle_parity_and_symmetry(nsd):
     n = 48
     inp, pb, v, pi = newton_state(n, 7, 4)
     J = pb.jacobian(v, pi, "sv")
-    H = OA.setup(J, pb)
-    ctx = make_ctx(n)
+    H = OA.setup(J, pb, v=v, nullspace_dim=nsd)
+    ctx = make_ctx(n, nullspace_dim=nsd)
     ctx.set_inputs(inp)
     ctx.assemble_jacobian(v, pi.ravel(), want_csr=False)
     ctx.amg_setup()
@@ -129,14 +133,20 @@ def test_single_level_is_exact_solve():
     assert np.linalg.norm(J @ z - r) <= 1e-10 * np.linalg.norm(r)
 
 
+@pytest.mark.parametrize("nsd,method", [(3, 0), (4, 0), (4, 1)])
 @pytest.mark.parametrize("n,it", [(32, 0), (32, 5), (64, 8)])
-def test_amg_fgmres_counts_parity(n, it):
+def test_amg_fgmres_counts_parity(n, it, nsd, method):
+    """AMG-FGMRES (krylov_method 0) and AMG-PCG (1) iteration counts vs the oracle's same
+    definitions, with 3 or 4 near-nullspace columns (reading G30)."""
     inp, pb, v, pi = newton_state(n, 11, it)
     J = pb.jacobian(v, pi, "sv")
     R = pb.residual(v)
-    H = OA.setup(J, pb)
-    xo, so = krylov.fgmres(lambda x: J @ x, R, lambda r: OA.vcycle(H, r), 30, 1e-8, 300)
-    ctx = make_ctx(n)
+    H = OA.setup(J, pb, v=v, nullspace_dim=nsd)
+    if method == 0:
+        xo, so = krylov.fgmres(lambda x: J @ x, R, lambda r: OA.vcycle(H, r), 30, 1e-8, 300)
+    else:
+        xo, so = krylov.pcg(lambda x: J @ x, R, lambda r: OA.vcycle(H, r), 1e-8, 300)
+    ctx = make_ctx(n, nullspace_dim=nsd, krylov_method=method)
     ctx.set_inputs(inp)
     ctx.assemble_jacobian(v, pi.ravel(), want_csr=False)
     ctx.amg_setup()

@@ -1,0 +1,97 @@
+"""Full-step parity at BASELINE.json configs 2 and 3 against stored oracle results.
+
+The goldens under tests/golden/ were written by scripts/make_goldens.py, which calls only
+`oracle/` (and the seeded generators): nothing stored there comes from the CUDA path.
+
+  cfg2  all 24 implicit steps of config 2 (n = 256, moving cyclone), oracle sv-Newton to 1e-8
+        with sparse direct solves, each step warm-started from the oracle's own v^n.  The GPU
+        runs the product path (AMG-FGMRES, default parameters) warm-started from its own v^n.
+  cfg3  step 1 of config 3 (n = 1024) with the oracle's AMG-FGMRES (tier B: the same AMG
+        definition as the GPU), so FGMRES counts are comparable too.
+
+Tolerances (BASELINE.json north_star): converged velocity per step 1e-8 relative L2, Newton
+count +-1, FGMRES count +-10 % (only against the same preconditioner definition, cfg3).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2204_10822_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _load(name):
+    p = os.path.join(GOLD, name)
+    if not os.path.exists(p):
+        pytest.fail(f"golden {name} missing: run scripts/make_goldens.py")
+    return p
+
+
+def test_cfg2_all_24_steps_match_oracle():
+    meta = json.load(open(_load("cfg2_steps.json")))
+    full = np.load(_load("cfg2_v.npz"))
+    from paper_2204_10822_b200.seaice import SeaIce
+    cfg = wl.CONFIGS[2]
+    assert meta["n"] == cfg.n and len(meta["steps"]) == cfg.steps
+    idx = np.asarray(meta["sample_idx"])
+    h, A = wl.ice_fields(cfg)
+    vo = wl.ocean_nodal(cfg.n)
+    ctx = SeaIce(cfg.n)
+    v = torch.zeros(2 * (cfg.n + 1) ** 2, dtype=torch.float64, device="cuda")
+    worst = {"sample": 0.0, "full": 0.0, "newton": 0}
+    for s, rec in enumerate(meta["steps"]):
+        va = wl.wind_nodal(cfg.n, (s + 1) * cfg.dt, cfg.moving)
+        v_new, st = ctx.solve_step(cfg.dt, (s + 1) * cfg.dt, h, A, v, va, vo)
+        assert st["converged"] == 1 and st["krylov_capped"] == 0, (s + 1, st)
+        assert abs(st["newton_iters"] - rec["newton"]) <= 1, (s + 1, st["newton_iters"], rec["newton"])
+        vg = v_new.cpu().numpy()
+        vs = np.asarray(rec["v_sample"])
+        es = np.linalg.norm(vg[idx] - vs) / np.linalg.norm(vs)
+        assert es <= 1e-8, (s + 1, es)
+        worst["sample"] = max(worst["sample"], es)
+        worst["newton"] = max(worst["newton"], abs(st["newton_iters"] - rec["newton"]))
+        key = f"v_step{s + 1}"
+        if key in full.files:
+            ref = full[key]
+            ef = np.linalg.norm(vg - ref) / np.linalg.norm(ref)
+            assert ef <= 1e-8, (s + 1, ef)
+            worst["full"] = max(worst["full"], ef)
+        v = v_new
+    print("cfg2 parity", worst)
+
+
+def test_cfg3_step1_matches_oracle_tier_b():
+    meta = json.load(open(_load("cfg3_step1.json")))
+    ref = np.load(_load("cfg3_v.npz"))["v_step1"]
+    from paper_2204_10822_b200.seaice import SeaIce
+    cfg = wl.CONFIGS[3]
+    inp = wl.step_inputs(cfg, 0)
+    ctx = SeaIce(cfg.n, **meta.get("gpu_params", {}))
+    v, st = ctx.solve_step(inp.dt, inp.t_new, inp.h, inp.A, inp.v_prev, inp.v_air, inp.v_ocean)
+    assert st["converged"] == 1, st
+    assert abs(st["newton_iters"] - meta["newton"]) <= 1, (st["newton_iters"], meta["newton"])
+    err = np.linalg.norm(v.cpu().numpy() - ref) / np.linalg.norm(ref)
+    assert err <= 1e-8, err
+    # FGMRES count per solve against the same AMG definition (the Newton paths coincide while
+    # the iterates agree; compare the solves both sides performed)
+    v0 = torch.zeros_like(v)
+    ctx2 = SeaIce(cfg.n, **meta.get("gpu_params", {}))
+    ctx2.set_step(inp.dt, inp.t_new, inp.h, inp.A, v0, inp.v_air, inp.v_ocean)
+    its = []
+    vv = v0.clone()
+    for _ in range(len(meta["krylov"])):
+        d = ctx2.newton_step(vv)
+        if d["converged_on_entry"]:
+            break
+        its.append(d["krylov"]["iters"])
+    m = min(len(its), len(meta["krylov"]))
+    tot_g, tot_o = sum(its[:m]), sum(meta["krylov"][:m])
+    assert abs(tot_g - tot_o) <= 0.10 * tot_o, (its, meta["krylov"])
+    bad = [(k, g, o) for k, (g, o) in enumerate(zip(its[:m], meta["krylov"][:m])) if abs(g - o) > max(0.10 * o, 1)]
+    assert len(bad) <= max(1, m // 5), bad
+    print("cfg3 parity", {"err": err, "newton": (st["newton_iters"], meta["newton"]), "krylov": (its, meta["krylov"])})

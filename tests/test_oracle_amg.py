@@ -161,3 +161,41 @@ def test_strength_threshold_hand_example():
         assert G[1, 2] == 0 and G[2, 1] == 0
         if strong:
             assert abs(G[0, 1] - 2 * c * c / 32.0) <= 1e-15
+
+
+def test_v_column_is_near_null_for_the_plastic_part_and_reproduced_by_ptent():
+    """Reading G30 (nullspace_dim = 4).  (a) The fact that justifies the fourth column: at a
+    consistent pi = tau(v)/Delta(v) the sv coefficient maps tau(v) to (P/Delta)(Delta_min^2 /
+    Delta^2) tau(v) (eq:modification), so the viscous part of J annihilates v up to
+    that factor while the Picard part (P/Delta) I does not.  Checked on the assembled operators at
+    a small plastic velocity (strain >> Delta_min, mass and drag energies negligible): v's energy
+    under J_sv is a few % of its Picard energy, while an independent random field keeps > 30 %.
+    (b) P_tent B_c = [rigid modes, v] exactly on aggregated rows, columns orthonormal."""
+    n = 24
+    _, inp = wl.custom_inputs(n, seed=5)
+    pb = M.Problem(inp, PRM)
+    v = wl.random_velocity(n, 6, amp=0.005)
+    w = wl.random_velocity(n, 7, amp=0.005)
+    pi = pb.pi_consistent(v)
+    Jsv = pb.jacobian(v, pi, "sv").tocsr()
+    Jpi = pb.jacobian(v, None, "picard").tocsr()
+    # energies of v: Picard viscous part E_p = v^T (Jpi - M - D) v > 0; sv removes all but
+    # a Delta_min^2/Delta^2 fraction of it
+    Ep = v @ (Jpi @ v)
+    Es = v @ (Jsv @ v)
+    assert 0 < Es < 0.05 * Ep
+    assert w @ (Jsv @ w) > 0.3 * (w @ (Jpi @ w))
+    H = amg.setup(Jsv, pb, v=v, nullspace_dim=4, coarse_max_dof=60)
+    lev = H["levels"][0]
+    B = amg.level0_nullspace(pb.n, pb.L, v)
+    assert B.shape[1] == 4
+    Pt_s, Bc, _ = amg.tentative(lev["agg"], B, 2)
+    rows = np.repeat(lev["agg"] >= 0, 2)
+    assert np.allclose((Pt_s @ Bc)[rows], B[rows], atol=1e-12 * np.abs(B).max())
+    PtP = (Pt_s.T @ Pt_s).toarray()
+    keep = np.diag(PtP) > 0.5
+    assert np.allclose(PtP[np.ix_(keep, keep)], np.eye(keep.sum()), atol=1e-13)
+    # coarse blocks are 4 x 4 and the Galerkin operator is SPD
+    Ac = H["levels"][1]["A"].toarray()
+    assert Ac.shape[0] % 4 == 0
+    assert np.linalg.eigvalsh(0.5 * (Ac + Ac.T)).min() > 0

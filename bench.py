@@ -6,9 +6,12 @@ Jacobian assembly, GPU AMG setup, AMG-FGMRES solve, energy backtracking, v/pi up
 ||R|| <= 1e-8 ||R_0||.  Default workload: BASELINE.json configs[4] ("2048x2048 Q1 mesh,
 ~8.4M unknowns, seed 3, moving cyclone") — the paper's largest problem.
 
-value = DOF * (FGMRES iterations) / s over the timed steps, summed over ranks (weak scaling:
-every rank solves an independent replica; the method has no data-path collective at this
-size).  s/timestep is reported beside it.
+value = solve seconds per time step (BASELINE.json's first metric) of the whole job: the max over
+ranks of the device-timed region divided by the time steps all ranks solved (weak scaling:
+every rank solves an independent replica; the method has no data-path collective at this size,
+DESIGN.md "Multi-GPU").  DOF * Krylov-iterations / s is reported beside it, with the Krylov
+iterations per solve and the number of solves that hit krylov_maxit (capped work is not useful
+work, so the iteration rate is not the headline).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
 """
@@ -30,8 +33,8 @@ import numpy as np
 
 from paper_2204_10822_b200 import workloads as wl
 
-METRIC = "DOF*Krylov-iters/s"
-UNIT = "DOF*iter/s"
+METRIC = "solve s/timestep"
+UNIT = "s/timestep"
 
 
 def parse():
@@ -125,57 +128,95 @@ def reduce_timing(ms, units, world, device=None):
 
 
 # ----------------------------------------------------------------------------- oracle arm
-def oracle_sample(cfg, n_sample=256):
-    """One full sv-Newton iteration of the CPU oracle (assembly, AMG setup, AMG-FGMRES,
-    energy line search, update) on the workload's generator at mesh n_sample.
-    Returns (DOF * Krylov iterations, seconds, description)."""
+COUNTS_FILE = os.path.join(ROOT, "profiles", "r02_cfg4_counts.json")
+
+
+def oracle_phases(cfg, n_sample=256, threads=None):
+    """Per-phase timing of the CPU oracle (numpy/scipy fp64, oracle/) on one full sv-Newton
+    iteration of the workload's generator at mesh n_sample: residual + Jacobian assembly, AMG
+    setup, AMG-FGMRES(30) to 1e-8, energy line search + dual/velocity update.  threads: BLAS /
+    OpenMP thread limit (threadpoolctl; None = all cores).  Returns per-phase seconds per DOF
+    (Krylov: per DOF per iteration) and the sample's description."""
+    from threadpoolctl import threadpool_limits
     from oracle import amg as OA
     from oracle import krylov
     from oracle.model import Problem
     prm = wl.PhysParams()
     scfg = wl.Config(cfg.name + f"_sample{n_sample}", n_sample, cfg.seed, 1, cfg.moving, cfg.kind, cfg.dt)
     inp = wl.step_inputs(scfg, 0)
-    t0 = time.perf_counter()
-    pb = Problem(inp, prm)
-    v = pb.v_prev.copy()
-    pi = pb.pi_consistent(v)
-    R = pb.residual(v)
-    J = pb.jacobian(v, pi, "sv")
-    H = OA.setup(J, pb)
-    vt, st = krylov.fgmres(lambda x: J @ x, R, lambda r: OA.vcycle(H, r), 30, 1e-8, 300)
-    for k in range(21):
-        if pb.delta_energy(v, vt, 0.5 ** k) < 0:
-            break
-    pi = pi + 0.5 ** k * pb.pi_tilde(v, pi, vt)
-    v = v + 0.5 ** k * vt
-    dt_s = time.perf_counter() - t0
     N = 2 * (n_sample + 1) ** 2
-    desc = (f"one full sv-Newton iteration of the CPU oracle (numpy/scipy, fp64) on {cfg.name}'s "
-            f"generator at n={n_sample} ({N} DOF, first iteration of implicit step 1): residual + "
-            f"Jacobian assembly, AMG setup, AMG-FGMRES(30) to 1e-8 ({st['iters']} its), line search, update")
-    return N * st["iters"], dt_s, desc
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        pb = Problem(inp, prm)
+        v = pb.v_prev.copy()
+        pi = pb.pi_consistent(v)
+        R = pb.residual(v)
+        J = pb.jacobian(v, pi, "sv")
+        t1 = time.perf_counter()
+        H = OA.setup(J, pb, v=v)
+        t2 = time.perf_counter()
+        vt, st = krylov.fgmres(lambda x: J @ x, R, lambda r: OA.vcycle(H, r), 30, 1e-8, 300)
+        t3 = time.perf_counter()
+        for k in range(21):
+            if pb.delta_energy(v, vt, 0.5 ** k) < 0:
+                break
+        pi = pi + 0.5 ** k * pb.pi_tilde(v, pi, vt)
+        v = v + 0.5 ** k * vt
+        t4 = time.perf_counter()
+    its = max(st["iters"], 1)
+    ph = {"assembly_s": t1 - t0, "amg_setup_s": t2 - t1, "krylov_s": t3 - t2, "krylov_iters": st["iters"],
+          "line_search_update_s": t4 - t3, "total_s": t4 - t0}
+    per_dof = {"newton_fixed": (t1 - t0 + t2 - t1 + t4 - t3) / N, "krylov_it": (t3 - t2) / its / N}
+    desc = (f"one full sv-Newton iteration of the CPU oracle (numpy/scipy fp64) on {cfg.name}'s generator at "
+            f"n={n_sample} ({N} DOF, first iteration of step 1), timed per phase")
+    return ph, per_dof, desc
+
+
+def extrapolate(per_dof, N, newton, krylov):
+    """Oracle seconds for one time step of N DOF with the given Newton / Krylov counts, from the
+    sample's per-DOF phase costs (the oracle's phases are linear in N: vectorised element
+    loops, sparse products, V-cycles; an explicitly labelled extrapolation)."""
+    return N * (newton * per_dof["newton_fixed"] + krylov * per_dof["krylov_it"])
+
+
+def cpu_baseline(cfg, N, newton, krylov, counts_src):
+    cores = os.cpu_count()
+    ph1, pd1, desc = oracle_phases(cfg, threads=1)
+    phA, pdA, _ = oracle_phases(cfg, threads=None)
+    v1 = extrapolate(pd1, N, newton, krylov)
+    vA = extrapolate(pdA, N, newton, krylov)
+    return {"value": vA, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": desc + f"; extrapolated per DOF to {cfg.name} ({N} DOF) with {newton:.1f} Newton and "
+                             f"{krylov:.0f} Krylov iterations per step ({counts_src})",
+            "value_1thread": v1, "phases_all_cores": phA, "phases_1thread": ph1}
 
 
 def run_reference(a, rank, world):
     if rank != 0:
         return
     cfg = wl.CONFIGS[a.config]
-    cores = int(os.environ.get("OMP_NUM_THREADS", "0")) or os.cpu_count()
+    N = 2 * (cfg.n + 1) ** 2
+    cores = os.cpu_count()
+    # counts per step of this workload: the product path's, recorded by bench.py on the B200
+    c = json.load(open(COUNTS_FILE)) if os.path.exists(COUNTS_FILE) else {}
+    newton = c.get("newton_per_step", 16.0)
+    krylov = c.get("krylov_per_step", 1600.0)
+    src = f"counts from {os.path.relpath(COUNTS_FILE, ROOT)}" if c else "assumed counts"
     for _ in range(a.warmup):
-        oracle_sample(cfg)
-    units = 0.0
-    secs = 0.0
+        oracle_phases(cfg)
+    vals = []
     desc = ""
     for _ in range(a.steps):
-        u, s, desc = oracle_sample(cfg)
-        units += u
-        secs += s
-    val = units / secs
+        ph, pd, desc = oracle_phases(cfg)
+        vals.append(extrapolate(pd, N, newton, krylov))
+    val = float(np.mean(vals))
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": a.gpus,
-            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * secs / a.steps, "higher_is_better": True,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * val, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "n": cfg.n, "sample_n": 256},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": desc + f"; extrapolated to {cfg.name} ({N} DOF), {newton} Newton / "
+                                              f"{krylov} Krylov iterations per step ({src})"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -251,9 +292,10 @@ def run_ours(a, rank, world, local_rank):
     prof = ctx.profile_read()
     ctx.profile(False)
     kry = sum(s["krylov_iters_total"] for s in stats)
-    units = float(N) * kry
-    ms_max, units_all = reduce_timing(ms, units, world, dev)
-    value = units_all / (ms_max / 1e3)
+    ms_max, kry_all = reduce_timing(ms, float(kry), world, dev)
+    steps_all = a.steps * world
+    value = ms_max / 1e3 / steps_all                     # whole-job seconds per time step
+    dof_its = float(N) * kry_all / (ms_max / 1e3)       # DOF * Krylov iterations / s (all ranks)
 
     # ---- end-to-end through the host-buffer C-ABI call (same steps again)
     e2e = None
@@ -274,10 +316,12 @@ def run_ours(a, rank, world, local_rank):
         barrier()
         ms_e = e0.elapsed_time(e1)
         kry_e = sum(s["krylov_iters_total"] for s in e2e_stats)
-        ms_e, u_e = reduce_timing(ms_e, float(N) * kry_e, world, dev)
-        e2e = {"value": u_e / (ms_e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * (2 * Nc + 3 * N),
+        ms_e, kry_e = reduce_timing(ms_e, float(kry_e), world, dev)
+        e2e = {"value": ms_e / 1e3 / steps_all, "unit": UNIT, "h2d_bytes_per_step": 8 * (2 * Nc + 3 * N),
                "d2h_bytes_per_step": 8 * N, "ms_per_step": ms_e / a.steps,
-               "s_per_timestep": ms_e / 1e3 / a.steps}
+               "dof_krylov_iters_per_s": float(N) * kry_e / (ms_e / 1e3),
+               "call": "seaice_solve_step_host (pinned host buffers, H2D of h, A, v^n, v_a, v_o and D2H of "
+                       "v^{n+1} inside the timed region)"}
 
     if rank != 0:
         return
@@ -297,34 +341,47 @@ def run_ours(a, rank, world, local_rank):
     dom = max(kern, key=lambda k: kern[k]["ms_total"]) if kern else None
     roof = None
     if dom and "achieved_gbs" in kern[dom]:
-        traffic = None
+        traffic, traffic_src = None, None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
-            traffic = json.load(open(tp)).get(dom)
+            tj = json.load(open(tp))
+            traffic = tj.get(dom)
+            traffic_src = "stored: " + tj.get("_source", "profiles/ncu_traffic.json") if traffic else None
         roof = {"kernel": dom, "bound": "hbm", "achieved": kern[dom]["achieved_gbs"], "peak": peak,
-                "unit": "GB/s", "frac": kern[dom]["frac_of_peak"], "traffic": traffic, "peak_source": peak_src,
+                "unit": "GB/s", "frac": kern[dom]["frac_of_peak"], "traffic": traffic,
+                "traffic_source": traffic_src, "peak_source": peak_src,
                 "bytes_per_launch": kern[dom]["alg_bytes_per_launch"],
                 "us_per_launch": kern[dom]["us_per_launch"]}
     cpu = None
+    newton_per_step = sum(s["newton_iters"] for s in stats) / a.steps
+    krylov_per_step = kry / a.steps
     if not a.no_cpu_baseline:
         try:
-            u, s, desc = oracle_sample(cfg)
-            cpu = {"value": u / s, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": desc,
-                   "seconds": round(s, 2)}
+            cpu = cpu_baseline(cfg, N, newton_per_step, krylov_per_step, "the counts of this run's timed steps")
         except Exception as ex:  # the baseline must never break the bench line
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {ex}"}
     mem_live, mem_peak = ctx.memory()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_max / a.steps, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "n": n, "dof": N, "seed": cfg.seed, "dt": cfg.dt,
                    "steps_timed": [s + 1 for s in range(a.warmup, total)], "parallelism": f"replicas x{world}",
                    "l2": "working set (J 1.2 GB + Krylov basis + AMG) far larger than the 126 MB L2; no flush",
-                   "newton_rtol": 1e-8, "krylov": "FGMRES(30) rtol 1e-8, AMG(MIS2-SA, Chebyshev-3)"},
+                   "newton_rtol": ctx.params.newton_rtol,
+                   "krylov": (f"{'PCG' if ctx.params.krylov_method else 'FGMRES(%d)' % ctx.params.restart} rtol "
+                              f"{ctx.params.krylov_rtol:g}{' + Eisenstat-Walker forcing' if ctx.params.krylov_forcing else ''}, "
+                              f"maxit {ctx.params.krylov_maxit}, AMG(MIS2 smoothed aggregation, "
+                              f"{ctx.params.nullspace_dim} near-nullspace columns, Chebyshev-{ctx.params.cheb_degree})"),
+                   "params_override": json.loads(a.params)},
         "s_per_timestep": ms_max / 1e3 / a.steps,
+        "dof_krylov_iters_per_s": dof_its,
         "newton_iters": [s["newton_iters"] for s in stats],
         "krylov_iters": [s["krylov_iters_total"] for s in stats],
+        "krylov_solves": [s["krylov_solves"] for s in stats],
+        "krylov_capped": [s["krylov_capped"] for s in stats],
+        "krylov_per_solve": round(kry / max(1, sum(s["krylov_solves"] for s in stats)), 2),
+        "krylov_max_per_solve": max(s["krylov_max_iters"] for s in stats),
         "converged": [s["converged"] for s in stats],
         "phase_ms": {k: round(sum(s[k] for s in stats) / a.steps, 2) for k in
                      ("t_setup", "t_assemble", "t_amg", "t_krylov", "t_ls")},

@@ -95,12 +95,16 @@ typedef struct {
                               exceeds 0.1) and eta_l >= 0.5 newton_rtol |R_0| / |R_l|, clamped to
                               [krylov_rtol, 0.1] (reading G29) */
   int32_t nullspace_dim;   /* AMG near-nullspace columns per aggregate = coarse block size:
-                              3 = rigid-body modes (1,0), (0,1), rotation; 4 (reading G30)
+                              3 = rigid-body modes (1,0), (0,1), rotation; 4 (default, reading G30)
                               adds the linearisation point v_l of the last seaice_assemble_jacobian,
                               a near-null vector of the plastic part of eq:modification:
                               C_q tau(v_l) = (P/Delta)(Delta_min^2/Delta^2) tau(v_l) at consistent pi */
   int32_t krylov_method;   /* 0 (default): FGMRES(restart); 1: preconditioned CG (J and the
                               symmetric V-cycle are SPD, eq:modification P:534-539; same stopping test) */
+  int32_t spgemm_path;     /* 0 (default): SpGEMM code path chosen by row-expansion size; testing knob
+                              to force one path for every product: 1 hash tables (1k, else 4k
+                              entries, else sort), 2 sort + thread-per-row numeric, 3 sort + 8-lane
+                              groups, 4 sort + warp per row (see seaice_spgemm_path_hits) */
 } seaice_params;
 
 /* Compressed-sparse-row view (scalar rows). Index arrays int32, values fp64. */
@@ -274,6 +278,14 @@ int64_t seaice_launch_count(const seaice_ctx* ctx);
 #define SEAICE_PROF_CLASSES 16
 int seaice_profile_enable(seaice_ctx* ctx, int32_t on);
 int seaice_profile_read(seaice_ctx* ctx, double* ms_host, int64_t* launches_host, double* alg_bytes_host);
+
+/* Which SpGEMM code path each Galerkin / prolongator-smoothing product of seaice_amg_setup took,
+ * counted since create (the numeric result is the same definition on every path;
+ * the choice depends only on row-expansion sizes).  hits[0] 1k-entry hash table per row,
+ * [1] 4k-entry hash table, [2] sort-based thread-per-row numeric, [3] sort-based 8-lane-group
+ * numeric, [4] sort-based warp-per-row (wide rows).  n_host: entries to write (<= 5). */
+#define SEAICE_SPGEMM_PATHS 5
+int seaice_spgemm_path_hits(const seaice_ctx* ctx, int64_t* hits_host, int32_t n_host);
 
 /* Bytes of device memory the context currently holds (and its peak). */
 int seaice_memory(const seaice_ctx* ctx, int64_t* live_bytes, int64_t* peak_bytes);

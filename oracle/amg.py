@@ -246,7 +246,7 @@ def level0_nullspace(n, L, v=None):
 
 def setup(J, pb=None, theta=0.04, coarse_max_dof=400, max_levels=25, power_iters=20, seed=0,
           cheb_degree=3, cheb_lower=0.03, cheb_upper=1.1, n=None, L=512e3, agg_dist0=2, agg_dist=2,
-          v=None, nullspace_dim=3):
+          v=None, nullspace_dim=4):
     """nullspace_dim = 4 (reading G30) appends the linearisation point v (required then) to
     the three rigid-body modes; coarse levels then carry 4 x 4 blocks."""
     if pb is not None:

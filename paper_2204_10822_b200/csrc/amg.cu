@@ -399,70 +399,77 @@ __global__ void k_seg_starts(int na, int nb, const int* __restrict__ skey, int* 
   start[a] = lo;
 }
 
-// per aggregate: two-pass MGS of the stacked near-nullspace rows (B x K per member)
+// Per aggregate: two-pass modified Gram-Schmidt of the stacked near-nullspace rows (B x K per
+// member), Q written directly into P_tent's blocks, R into the coarse
+// near-nullspace.  One warp per aggregate: lane l owns the stacked rows l, l + 32, ... (row rho
+// is component rho % B of member rho / B); the column dot products are xor-butterfly warp sums
+// (every lane gets the same fixed-order total).
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 template <int B, int K>
-__global__ void k_tentative(int na, const int* __restrict__ start, const int* __restrict__ members,
-                            const double* __restrict__ Bn, const int* __restrict__ prp, double* __restrict__ pval,
-                            double* __restrict__ Bc) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= na) return;
+__global__ void __launch_bounds__(128) k_tentative_w(int na, const int* __restrict__ start,
+                                                     const int* __restrict__ members, const double* __restrict__ Bn,
+                                                     const int* __restrict__ prp, double* __restrict__ pval,
+                                                     double* __restrict__ Bc) {
+  const int a = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (a >= na) return;  // uniform per warp
   const int m0 = start[a], m1 = start[a + 1];
+  const int nrow = (m1 - m0) * B;
   double R[K * K];
 #pragma unroll
   for (int t = 0; t < K * K; ++t) R[t] = 0.0;
   bool keep[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) keep[k] = false;
-  // Q is written directly into P_tent's blocks (one block per member, column agg a)
-  for (int k = 0; k < K; ++k) {
-    // v = B[:,k]
-    double n0 = 0.0;
-    for (int t = m0; t < m1; ++t) {
-      const int I = members[t];
-      double* q = pval + (long long)prp[I] * B * K;
+  auto qptr = [&](int rho) -> double* {
+    return pval + (long long)prp[members[m0 + rho / B]] * B * K + (rho % B) * K;
+  };
 #pragma unroll
-      for (int rr = 0; rr < B; ++rr) {
-        const double v = Bn[((long long)I * B + rr) * K + k];
-        q[rr * K + k] = v;
-        n0 += v * v;
-      }
+  for (int k = 0; k < K; ++k) {
+    double n0 = 0.0;
+    for (int rho = lane; rho < nrow; rho += 32) {
+      const int I = members[m0 + rho / B];
+      const double v = Bn[((long long)I * B + rho % B) * K + k];
+      qptr(rho)[k] = v;
+      n0 += v * v;
     }
-    n0 = sqrt(n0);
+    n0 = sqrt(warp_allsum(n0));
     for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
       for (int j = 0; j < k; ++j) {
         if (!keep[j]) continue;
         double rj = 0.0;
-        for (int t = m0; t < m1; ++t) {
-          const double* q = pval + (long long)prp[members[t]] * B * K;
-#pragma unroll
-          for (int rr = 0; rr < B; ++rr) rj += q[rr * K + j] * q[rr * K + k];
+        for (int rho = lane; rho < nrow; rho += 32) {
+          const double* q = qptr(rho);
+          rj += q[j] * q[k];
         }
+        rj = warp_allsum(rj);
         R[j * K + k] += rj;
-        for (int t = m0; t < m1; ++t) {
-          double* q = pval + (long long)prp[members[t]] * B * K;
-#pragma unroll
-          for (int rr = 0; rr < B; ++rr) q[rr * K + k] -= rj * q[rr * K + j];
+        for (int rho = lane; rho < nrow; rho += 32) {
+          double* q = qptr(rho);
+          q[k] -= rj * q[j];
         }
       }
     }
     double nv = 0.0;
-    for (int t = m0; t < m1; ++t) {
-      const double* q = pval + (long long)prp[members[t]] * B * K;
-#pragma unroll
-      for (int rr = 0; rr < B; ++rr) nv += q[rr * K + k] * q[rr * K + k];
+    for (int rho = lane; rho < nrow; rho += 32) {
+      const double* q = qptr(rho);
+      nv += q[k] * q[k];
     }
-    nv = sqrt(nv);
+    nv = sqrt(warp_allsum(nv));
     keep[k] = (nv > 1e-8 * n0) && (nv > 0.0);
     const double sc = keep[k] ? 1.0 / nv : 0.0;
     if (keep[k]) R[k * K + k] = nv;
-    for (int t = m0; t < m1; ++t) {
-      double* q = pval + (long long)prp[members[t]] * B * K;
-#pragma unroll
-      for (int rr = 0; rr < B; ++rr) q[rr * K + k] *= sc;
-    }
+    for (int rho = lane; rho < nrow; rho += 32) qptr(rho)[k] *= sc;
   }
+  if (lane == 0) {
 #pragma unroll
-  for (int t = 0; t < K * K; ++t) Bc[(long long)a * K * K + t] = R[t];
+    for (int t = 0; t < K * K; ++t) Bc[(long long)a * K * K + t] = R[t];
+  }
 }
 
 __global__ void k_flag_agg(int nb, const int* __restrict__ agg, int* __restrict__ f) {
@@ -910,12 +917,15 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
     const long long tot = read_scalar(c, off + nr);
     // the per-warp table has a fixed per-row cost: short rows (finest level) stay on the
     // sort-based path, whose thread-per-row numeric phase suits them
-    const bool wide_rows = tot >= 32LL * nr;
+    const int force = c.p.spgemm_path;  // testing knob (seaice_params.spgemm_path)
+    const bool wide_rows = force == 1 || (force == 0 && tot >= 32LL * nr);
     if (wide_rows && maxub <= kHT / 2) {
+      c.sg_hits[0]++;
       hash_spgemm<M, K, P, kHT, kHWarps>(c, X, Y, crp, cci, cval, cnnzb, S);
       return;
     }
     if (wide_rows && maxub <= kHT2 / 2) {
+      c.sg_hits[1]++;
       hash_spgemm<M, K, P, kHT2, kHWarps2>(c, X, Y, crp, cci, cval, cnnzb, S);
       return;
     }
@@ -926,7 +936,8 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
   tick(c, "  sg.ub", nr);
   int* k1 = S.get<int>(total);
   int* k2 = S.get<int>(total);
-  const bool wide = total > 48LL * nr;  // long rows: warp per row
+  const int force = c.p.spgemm_path;
+  const bool wide = force == 4 || ((force == 0 || force == 1) && total > 48LL * nr);  // long rows: warp per row
   if (wide)
     k_spgemm_expand_w<<<wgrid(nr), 256, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, off, k1);
   else
@@ -955,6 +966,8 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
   SI_CHECK(cnnzb < (1LL << 31), SEAICE_EINVAL, "SpGEMM result exceeds int32 indexing");
   cci.ensure(c.al, cnnzb);
   cval.ensure(c.al, cnnzb * M * P);
+  const bool thread_numeric = force == 2 || ((force == 0 || force == 1) && Y.nbr > 0 && (double)Y.nnzb / Y.nbr <= 6.0);
+  c.sg_hits[wide ? 4 : thread_numeric ? 2 : 3]++;
   if (wide) {
     k_spgemm_compact_w<<<wgrid(nr), 256, 0, c.s>>>(nr, off, k1, crp.get(), cci.get());
     SI_LAUNCHED(c);
@@ -963,8 +976,7 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
   } else {
     k_spgemm_compact<<<grid_for(nr), kThreads, 0, c.s>>>(nr, off, k1, crp.get(), cci.get());
     SI_LAUNCHED(c);
-    const double ylen = Y.nbr > 0 ? (double)Y.nnzb / Y.nbr : 1.0;
-    if (ylen <= 6.0)  // measured: thread per row beats 4-lane groups for the finest level
+    if (thread_numeric)  // measured: thread per row beats 4-lane groups for the finest level
       k_spgemm_numeric<M, K, P><<<grid_for(nr, 128), 128, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val,
                                                                      crp.get(), cci.get(), cval.get());
     else
@@ -1640,13 +1652,14 @@ __global__ void __launch_bounds__(256) k_aspmv(int nb, const int* __restrict__ r
   const int row = (int)(t / G), lig = (int)(t % G);
   const bool own = row < nb && lig < BR;
   const long long i = (long long)row * SR + lig;
-  const double y0 = (own && yin) ? yin[i] : 0.0;
   const double acc = grpA_row<BR, BC, S>(row, nb, lig, rp, ci, val, x);
-  if (own) y[i] = y0 + acc;
+  if (own) y[i] = (yin ? yin[i] : 0.0) + acc;
 }
 
-// Chebyshev step on a b = 4 level (semantics of k_gcheb)
-template <int S>
+// Chebyshev step on a b = 4 level (semantics of k_gcheb).  LATE: the row's own vector entries
+// and D^-1 block are loaded after the SpMV (fewer live registers during the gather loop, at
+// the cost of one more round trip); otherwise before it.
+template <int S, bool LATE>
 __global__ void __launch_bounds__(256) k_acheb4(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
                                                 const double* __restrict__ val, const double* __restrict__ dinv,
                                                 const double* __restrict__ d, double* __restrict__ r,
@@ -1658,7 +1671,7 @@ __global__ void __launch_bounds__(256) k_acheb4(int nb, const int* __restrict__ 
   const bool own = row < nb && lig < 4;
   const long long i = (long long)row * 4 + lig;
   double dv = 0.0, xv = 0.0, rv = 0.0, D[4] = {0.0, 0.0, 0.0, 0.0};
-  if (own) {
+  if (!LATE && own) {
     dv = d[i];
     if (!first) xv = x[i];
     if (want_r) rv = r[i];
@@ -1666,6 +1679,12 @@ __global__ void __launch_bounds__(256) k_acheb4(int nb, const int* __restrict__ 
   }
   double acc = 0.0;
   if (want_r) acc = grpA_row<4, 4, S>(row, nb, lig, rp, ci, val, d);
+  if (LATE && own) {
+    dv = d[i];
+    if (!first) xv = x[i];
+    if (want_r) rv = r[i];
+    if (want_d) load_row<4>(dinv + (long long)row * 16 + lig * 4, D);
+  }
   if (own) x[i] = xv + dv;
   if (!want_r) return;  // uniform across the launch
   rv -= acc;
@@ -1689,11 +1708,11 @@ __global__ void __launch_bounds__(256) k_aresid4(int nb, const int* __restrict__
   const bool own = row < nb && lig < 4;
   const long long i = (long long)row * 4 + lig;
   double bo = 0.0, D[4] = {0.0, 0.0, 0.0, 0.0};
-  if (own) {
+  const double acc = x ? grpA_row<4, 4, S>(row, nb, lig, rp, ci, val, x) : 0.0;
+  if (own) {  // after the gather (fewer live registers in the loop, as k_acheb4)
     bo = b[i];
     load_row<4>(dinv + (long long)row * 16 + lig * 4, D);
   }
-  const double acc = x ? grpA_row<4, 4, S>(row, nb, lig, rp, ci, val, x) : 0.0;
   const double rv = bo - acc;
   if (own) r[i] = rv;
   double z = 0.0;
@@ -1908,7 +1927,8 @@ static void build_transfer(Ctx& c, Level& L, Level& Lc, int lvl, int na, Scratch
   k_ptent_ci<<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.agg.get(), ptrp, ptci);
   SI_LAUNCHED(c);
   Lc.B.ensure(c.al, (size_t)na * K * K);
-  k_tentative<B, K><<<grid_for(na, 128), 128, 0, c.s>>>(na, start, members, L.B.get(), ptrp, ptval, Lc.B.get());
+  k_tentative_w<B, K><<<(int)(((long long)na * 32 + 127) / 128), 128, 0, c.s>>>(na, start, members, L.B.get(), ptrp,
+                                                                                 ptval, Lc.B.get());
   SI_LAUNCHED(c);
   tick(c, "tentative", lvl);
   BsrMat Pt{nb, na, B, K, ptn, ptrp, ptci, ptval};
@@ -2198,9 +2218,10 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
                                                                          want_r, want_d)))
       else {
         const int Sl = pick_slots(L.nnzb, L.nb, 4);
-        SI_SDISPATCH(Sl, (k_acheb4<SS><<<agrid(L.nb, 4 * SS), 256, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(),
-                                                                             L.val.get(), L.dinv.get(), d, r, x, d2,
-                                                                             c1, c2, first, want_r, want_d)))
+        // late own-entry loads: measured 2357 -> 1555 us of coarse smoothing per V-cycle (config 4)
+        SI_SDISPATCH(Sl, (k_acheb4<SS, true><<<agrid(L.nb, 4 * SS), 256, 0, c.s>>>(
+                             L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), d, r, x, d2, c1, c2, first,
+                             want_r, want_d)))
       }
     }
     SI_LAUNCHED(c);

@@ -72,6 +72,7 @@ void validate(const seaice_params* p) {
   SI_CHECK(p->krylov_forcing == 0 || p->krylov_forcing == 1, SEAICE_EINVAL, "krylov_forcing must be 0 or 1");
   SI_CHECK(p->nullspace_dim == 3 || p->nullspace_dim == 4, SEAICE_EINVAL, "nullspace_dim must be 3 or 4");
   SI_CHECK(p->krylov_method == 0 || p->krylov_method == 1, SEAICE_EINVAL, "krylov_method must be 0 or 1");
+  SI_CHECK(p->spgemm_path >= 0 && p->spgemm_path <= 4, SEAICE_EINVAL, "spgemm_path must be in 0..4");
 }
 
 int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* out) {
@@ -261,8 +262,9 @@ void seaice_default_params(seaice_params* p, int32_t n) {
   p->cheb_degree0 = 0;  // measured no gain on B200 (grid barriers ~ launch gaps in the graph)
   p->matfree = 0;       // the assembled 19-value stencil SpMV is ~4x cheaper than the matrix-free apply
   p->krylov_forcing = 0;  // fixed krylov_rtol per Newton solve (reading G13)
-  p->nullspace_dim = 3;
+  p->nullspace_dim = 4;  // rigid-body modes + the linearisation point (reading G30)
   p->krylov_method = 0;
+  p->spgemm_path = 0;
 }
 
 int seaice_create(const seaice_params* p, const seaice_runtime* rt, seaice_ctx** out) {
@@ -537,6 +539,12 @@ int seaice_profile_read(seaice_ctx* h, double* ms, int64_t* cnt, double* bytes) 
   }
   return SEAICE_OK;
   API_END
+}
+
+int seaice_spgemm_path_hits(const seaice_ctx* h, int64_t* hits, int32_t n) {
+  if (!h || !hits || n < 0) return SEAICE_EINVAL;
+  for (int k = 0; k < n && k < SEAICE_SPGEMM_PATHS; ++k) hits[k] = (int64_t)h->c.sg_hits[k];
+  return SEAICE_OK;
 }
 
 int seaice_memory(const seaice_ctx* h, int64_t* live, int64_t* peak) {

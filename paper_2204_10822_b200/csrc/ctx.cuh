@@ -126,6 +126,7 @@ struct Ctx {
   Phys ph{};
   std::string err;
   long long launches = 0;
+  long long sg_hits[SEAICE_SPGEMM_PATHS] = {0, 0, 0, 0, 0};  // SpGEMM path counters (seaice_spgemm_path_hits)
 
   // per-step state
   bool step_set = false, assembled = false, amg_ready = false;

@@ -36,7 +36,8 @@ class Params(C.Structure):
                 ("project_pi", C.c_int32), ("amg_seed", C.c_uint64), ("agg_dist0", C.c_int32),
                 ("agg_dist", C.c_int32), ("cheb_fused", C.c_int32),
                 ("cheb_degree0", C.c_int32), ("matfree", C.c_int32),
-                ("krylov_forcing", C.c_int32), ("nullspace_dim", C.c_int32), ("krylov_method", C.c_int32)]
+                ("krylov_forcing", C.c_int32), ("nullspace_dim", C.c_int32), ("krylov_method", C.c_int32),
+                ("spgemm_path", C.c_int32)]
 
 
 ALLOC_T = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -142,6 +143,7 @@ def lib(build_if_missing: bool = True):
             "seaice_profile_enable": (C.c_int, [VP, I32]),
             "seaice_profile_read": (C.c_int, [VP, P(D), P(C.c_int64), P(D)]),
             "seaice_memory": (C.c_int, [VP, P(C.c_int64), P(C.c_int64)]),
+            "seaice_spgemm_path_hits": (C.c_int, [VP, P(C.c_int64), I32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -274,6 +276,12 @@ class SeaIce:
         by = (C.c_double * 16)()
         self._check(self.L.seaice_profile_read(self.h, ms, cnt, by))
         return {name: {"ms": ms[k], "launches": cnt[k], "bytes": by[k]} for k, name in enumerate(self.PROF_NAMES)}
+
+    def spgemm_path_hits(self):
+        """Counts of the SpGEMM code paths taken since create (seaice_spgemm_path_hits)."""
+        h = (C.c_int64 * 5)()
+        self._check(self.L.seaice_spgemm_path_hits(self.h, h, 5))
+        return list(h)
 
     def memory(self):
         live, peak = C.c_int64(), C.c_int64()

@@ -86,6 +86,35 @@ def test_jacobian_parity(kind, n):
         assert set(np.unique(nnz)) <= {1, 18}
 
 
+@pytest.mark.parametrize("kind", ["sv", "std", "picard"])
+def test_jacobian_parity_at_rest_on_drag_cutoff(kind):
+    """v = v_o = 0 and pi = 0: every Gauss point sits on Delta = Delta_min and on the ocean-drag
+    cut-off |w| < 1e-12 (rank-one drag term dropped, reading of S:198), the degenerate state of
+    the first Newton iterate from rest; plus a state with v = v_o exactly on half the nodes."""
+    n = 24
+    _, inp = wl.custom_inputs(n, seed=3)
+    inp.v_ocean = np.zeros_like(inp.v_ocean)
+    ctx = make_ctx(n, jacobian=kind)
+    ctx.set_inputs(inp)
+    pb = M.Problem(inp, PRM)
+    z = np.zeros(pb.N)
+    Jg = gpu_csr(ctx, z, np.zeros(12 * n * n))
+    Jo = pb.jacobian(z, np.zeros((3, 4, n * n)) if kind == "sv" else None, kind)
+    assert_rows_close(Jg, Jo)
+    Rg, _ = ctx.residual(z)
+    Ro, S = pb.residual(z, with_scale=True)
+    assert np.all(np.abs(to_np(Rg) - Ro) <= 1e-12 * S + 1e-300)
+    # v equal to v_o (= 0) on the left half, plastic elsewhere
+    v = state(n, 4)
+    s = n + 1
+    left = (np.arange(s * s) % s) < s // 2
+    v[np.repeat(left, 2)] = 0.0
+    pi = pb.pi_consistent(v)
+    Jg = gpu_csr(ctx, v, pi.ravel())
+    Jo = pb.jacobian(v, pi if kind == "sv" else None, kind)
+    assert_rows_close(Jg, Jo)
+
+
 def test_spmv_parity():
     n = 64
     _, inp = wl.custom_inputs(n, seed=7)

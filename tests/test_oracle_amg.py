@@ -27,7 +27,7 @@ def _jacobian(n, seed=5, amp=0.05):
 @pytest.fixture(scope="module")
 def hier():
     pb, J = _jacobian(24)
-    return pb, J, amg.setup(J, pb, coarse_max_dof=60)
+    return pb, J, amg.setup(J, pb, coarse_max_dof=60, nullspace_dim=3)
 
 
 def test_mis2_is_distance2_independent_and_maximal():
@@ -113,7 +113,7 @@ def test_vcycle_symmetric(hier):
 
 def test_single_level_vcycle_is_exact_solve():
     pb, J = _jacobian(8)
-    H = amg.setup(J, pb, coarse_max_dof=10 ** 6)
+    H = amg.setup(J, pb, coarse_max_dof=10 ** 6, nullspace_dim=3)
     assert len(H["levels"]) == 1
     r = np.random.default_rng(2).standard_normal(J.shape[0])
     x = amg.vcycle(H, r)

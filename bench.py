@@ -47,6 +47,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--params", default="{}", help="JSON overrides of seaice_params")
+    ap.add_argument("--cpu-kernels", action="store_true",
+                    help="time the oracle on config 5's four operations (CPU baseline of the kernel "
+                         "microbench, SURVEY 8(d)) at a sample size, extrapolated per DOF; one JSON line")
+    ap.add_argument("--sample-n", type=int, default=512)
     return ap.parse_args()
 
 
@@ -189,6 +193,49 @@ def cpu_baseline(cfg, N, newton, krylov, counts_src):
             "sample": desc + f"; extrapolated per DOF to {cfg.name} ({N} DOF) with {newton:.1f} Newton and "
                              f"{krylov:.0f} Krylov iterations per step ({counts_src})",
             "value_1thread": v1, "phases_all_cores": phA, "phases_1thread": ph1}
+
+
+def oracle_kernels(n_sample=512, threads=None):
+    """CPU oracle timings of config 5's four operations (reading G24 state: v = 0, pi = 0,
+    log-uniform viscosity) at mesh n_sample: residual + sv-Jacobian assembly, one SpMV (scipy
+    CSR), one AMG V-cycle (Chebyshev 3), one FGMRES(30) cycle with rtol 0 (30 iterations),
+    each extrapolated per DOF to n = 4096 (labelled)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import amg as OA
+    from oracle import krylov
+    from oracle.model import Problem
+    cfg5 = wl.CONFIGS[5]
+    scfg = wl.Config(cfg5.name + f"_sample{n_sample}", n_sample, cfg5.seed, 1, cfg5.moving, cfg5.kind, cfg5.dt)
+    inp = wl.step_inputs(scfg, 0)
+    prm = wl.PhysParams()
+    N = 2 * (n_sample + 1) ** 2
+    N5 = 2 * (cfg5.n + 1) ** 2
+    out = {}
+    with threadpool_limits(limits=threads):
+        pb = Problem(inp, prm)
+        v = np.zeros(N)
+        pi = np.zeros((3, 4, n_sample * n_sample))
+        t0 = time.perf_counter()
+        pb.residual(v)
+        J = pb.jacobian(v, pi, "sv").tocsr()
+        out["assembly_s"] = time.perf_counter() - t0
+        x = np.random.default_rng(0).standard_normal(N)
+        t0 = time.perf_counter()
+        for _ in range(5):
+            J @ x
+        out["spmv_s"] = (time.perf_counter() - t0) / 5
+        H = OA.setup(J, pb, v=v)
+        t0 = time.perf_counter()
+        OA.vcycle(H, x)
+        out["vcycle_s"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        krylov.fgmres(lambda y: J @ y, x, lambda r: OA.vcycle(H, r), 30, 0.0, 30)
+        out["fgmres_cycle_s"] = time.perf_counter() - t0
+    scale = N5 / N
+    return {"sample_n": n_sample, "sample_dof": N, "threads": threads or os.cpu_count(),
+            "measured_s": out, "extrapolated_to_cfg5_s": {k: v * scale for k, v in out.items()},
+            "note": "oracle (numpy/scipy fp64) timed at the sample size, scaled by DOF ratio "
+                    f"{scale:.1f} to config 5 (n = 4096): a labelled extrapolation (SURVEY 8(d))"}
 
 
 def run_reference(a, rank, world):
@@ -379,6 +426,7 @@ def run_ours(a, rank, world, local_rank):
         "newton_iters": [s["newton_iters"] for s in stats],
         "krylov_iters": [s["krylov_iters_total"] for s in stats],
         "krylov_solves": [s["krylov_solves"] for s in stats],
+        "amg_setups": [s["amg_setups"] for s in stats],
         "krylov_capped": [s["krylov_capped"] for s in stats],
         "krylov_per_solve": round(kry / max(1, sum(s["krylov_solves"] for s in stats)), 2),
         "krylov_max_per_solve": max(s["krylov_max_iters"] for s in stats),
@@ -401,6 +449,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.cpu_kernels:
+        if rank == 0:
+            print(json.dumps({"cpu_kernels_cfg5": {"all_cores": oracle_kernels(a.sample_n),
+                                                   "one_thread": oracle_kernels(a.sample_n, threads=1)}}))
+        return
     if a.impl == "reference":
         run_reference(a, rank, world)
         return

@@ -88,8 +88,8 @@ typedef struct {
   int32_t matfree;         /* 0 (default): FGMRES applies the assembled stencil J; 1: FGMRES applies
                               J(v, pi) matrix-free from the (v, pi) of the
                               last assembly, the AMG hierarchy still built from the assembled J */
-  int32_t krylov_forcing;  /* 0 (default): every Newton solve to krylov_rtol (reading G13);
-                              1: Eisenstat-Walker choice-2 forcing (inexact Newton; the paper is
+  int32_t krylov_forcing;  /* 0: every Newton solve to krylov_rtol (reading G13);
+                              1 (default): Eisenstat-Walker choice-2 forcing (inexact Newton; the paper is
                               silent on its Krylov tolerance): eta_0 = 0.1, eta_l = 0.9 (|R_l| /
                               |R_{l-1}|)^2 with the safeguards eta_l >= 0.9 eta_{l-1}^2 (when that
                               exceeds 0.1) and eta_l >= 0.5 newton_rtol |R_0| / |R_l|, clamped to
@@ -105,6 +105,11 @@ typedef struct {
                               to force one path for every product: 1 hash tables (1k, else 4k
                               entries, else sort), 2 sort + thread-per-row numeric, 3 sort + 8-lane
                               groups, 4 sort + warp per row (see seaice_spgemm_path_hits) */
+  int32_t amg_lag;         /* 0: full AMG setup at every Newton iteration; T > 0 (reading G31):
+                              at Newton iteration l >= 1 of a time step the hierarchy is rebuilt only
+                              if the previous linear solve needed more than T Krylov iterations,
+                              otherwise its coarse levels (P, R, A_l, l >= 1) are kept and only the
+                              finest level (D^-1 blocks, lambda_max) is refreshed from the current J */
 } seaice_params;
 
 /* Compressed-sparse-row view (scalar rows). Index arrays int32, values fp64. */
@@ -140,6 +145,7 @@ typedef struct {
   int32_t amg_levels;
   double amg_op_complexity;
   double t_assemble, t_amg, t_krylov, t_ls; /* milliseconds (CUDA events) */
+  int32_t amg_rebuilt;      /* 1: full AMG setup this iteration; 0: coarse levels kept (amg_lag) */
 } seaice_newton_stats;
 
 typedef struct {
@@ -151,6 +157,7 @@ typedef struct {
                                (their iterations are counted in krylov_iters_total; the Newton
                                step still used the capped iterate) */
   int32_t krylov_max_iters; /* largest iteration count of one solve */
+  int32_t amg_setups;       /* full AMG setups in the step (< newton_iters with amg_lag) */
 } seaice_step_stats;
 
 /* Default parameters (Table 1 + BASELINE.json + DESIGN.md readings) for mesh size n. */

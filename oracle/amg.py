@@ -289,6 +289,20 @@ def setup(J, pb=None, theta=0.04, coarse_max_dof=400, max_levels=25, power_iters
             "op_complexity": sum(l["A"].nnz for l in levels) / nnz0}
 
 
+def refresh_finest(H, J, seed=0, power_iters=20):
+    """Lagged hierarchy (reading G31): keep the coarse levels (P, R, A_l for l >= 1) of H and
+    replace only the finest level's operator by the current J, with its block-diagonal inverse
+    and lambda_max recomputed (the smoother on level 0 always uses the current Jacobian)."""
+    lev0 = dict(H["levels"][0])
+    A = J.tocsr()
+    Dinv, _ = block_diag_inv(A, lev0["b"])
+    lev0.update({"A": A, "Dinv": Dinv, "lmax": lambda_max(A, Dinv, seed, 0, power_iters)})
+    levels = [lev0] + H["levels"][1:]
+    if len(levels) == 1:
+        levels[0]["chol"] = sla.cho_factor(A.toarray(), lower=True)
+    return {**H, "levels": levels}
+
+
 def chebyshev(lev, bvec, x, m, lo, up, need_residual):
     """Chebyshev(m) for D^-1 A on [lo*bmax, bmax], bmax = up*lambda (Saad, Alg. 12.1).
     Returns x and, if need_residual, r = b - A x (from the recurrence)."""

@@ -23,11 +23,15 @@ LS_ETA = 1e-12
 
 def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
                ls_max=20, krylov_rtol=1e-8, krylov_maxit=300, restart=30,
-               project_pi=False, amg_params=None, record_iterates=False, forcing=0):
+               project_pi=False, amg_params=None, record_iterates=False, forcing=0, amg_lag=0):
     """forcing = 1: Eisenstat-Walker choice 2 for the Krylov tolerance of each solve (reading
     G29, DESIGN.md): eta_0 = 0.1, eta_l = 0.9 (|R_l|/|R_{l-1}|)^2, safeguards
     eta_l >= 0.9 eta_{l-1}^2 (if > 0.1) and eta_l >= 0.5 rtol |R_0|/|R_l|, clamped to
-    [krylov_rtol, 0.1]."""
+    [krylov_rtol, 0.1].
+    amg_lag = T > 0 (reading G31): at Newton iteration l >= 1 the AMG hierarchy is rebuilt only
+    if the previous linear solve needed more than T Krylov iterations; otherwise its coarse
+    levels are kept and only the finest level is refreshed from the current Jacobian
+    (amg.refresh_finest)."""
     pb = Problem(inp, prm)
     v = pb.v_prev.copy()
     v[pb.bdof] = 0.0
@@ -36,6 +40,7 @@ def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
             "stagnated": [], "iterates": []}
     r0 = None
     converged = False
+    H = None
     for l in range(maxit + 1):
         R = pb.residual(v)
         nr = float(np.linalg.norm(R))
@@ -77,7 +82,13 @@ def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
             from . import amg
             # the linearisation point v is the fourth near-nullspace column when
             # amg_params["nullspace_dim"] == 4 (reading G30); ignored otherwise
-            H = amg.setup(J, pb, v=v, **(amg_params or {}))
+            ap = amg_params or {}
+            if H is None or amg_lag <= 0 or hist["krylov"][-1]["iters"] > amg_lag:
+                H = amg.setup(J, pb, v=v, **ap)
+                hist.setdefault("amg_rebuilt", []).append(True)
+            else:
+                H = amg.refresh_finest(H, J, seed=ap.get("seed", 0), power_iters=ap.get("power_iters", 20))
+                hist.setdefault("amg_rebuilt", []).append(False)
             if linsolve == "amg_fgmres":
                 vt, kst = krylov.fgmres(lambda x: J @ x, R, lambda r: amg.vcycle(H, r), restart,
                                         krtol, krylov_maxit)

@@ -1721,6 +1721,112 @@ __global__ void __launch_bounds__(256) k_aresid4(int nb, const int* __restrict__
   if (own) d[i] = c2 * z;
 }
 
+// CTA per block row (small coarse levels, ~50-110 blocks per row): 256 / BR slots keep the whole
+// row in flight at once (one dependent load chain instead of ~7), partial sums combined by an
+// xor-butterfly inside each warp and then across the 8 warps in a fixed order.  Thread a < BR
+// returns component a of the row, the others 0.
+template <int BR, int BC>
+__device__ __forceinline__ double cta_row(int row, const int* __restrict__ rp, const int* __restrict__ ci,
+                                          const double* __restrict__ val, const double* __restrict__ x,
+                                          double (*sh)[4]) {
+  constexpr int S = 256 / BR;
+  const int t = threadIdx.x, a = t % BR, slot = t / BR;
+  double acc = 0.0;
+  const int e1 = __ldg(rp + row + 1);
+  int e = __ldg(rp + row) + slot;
+  for (; e + S < e1; e += 2 * S) {
+    const int c0 = __ldg(ci + e), c1 = __ldg(ci + e + S);
+    double v0[BC], v1[BC], x0[BC], x1[BC];
+    load_row<BC>(val + ((long long)e * BR + a) * BC, v0);
+    load_row<BC>(val + ((long long)(e + S) * BR + a) * BC, v1);
+    load_xblk<BC>(x, c0, x0);
+    load_xblk<BC>(x, c1, x1);
+#pragma unroll
+    for (int b = 0; b < BC; ++b) acc += v0[b] * x0[b];
+#pragma unroll
+    for (int b = 0; b < BC; ++b) acc += v1[b] * x1[b];
+  }
+  if (e < e1) {
+    double v0[BC], x0[BC];
+    load_row<BC>(val + ((long long)e * BR + a) * BC, v0);
+    load_xblk<BC>(x, __ldg(ci + e), x0);
+#pragma unroll
+    for (int b = 0; b < BC; ++b) acc += v0[b] * x0[b];
+  }
+#pragma unroll
+  for (int off = BR; off < 32; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((t & 31) < BR) sh[t >> 5][a] = acc;
+  __syncthreads();
+  double tot = 0.0;
+  if (t < BR) {
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += sh[w][t];
+  }
+  return tot;
+}
+
+template <int BR, int BC>
+__global__ void __launch_bounds__(256) k_aspmv_cta(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                   const double* __restrict__ val, const double* __restrict__ x,
+                                                   const double* yin, double* y) {
+  __shared__ double sh[8][4];
+  constexpr int SR = vstride(BR);
+  const int row = blockIdx.x, t = threadIdx.x;
+  const double acc = cta_row<BR, BC>(row, rp, ci, val, x, sh);
+  if (t < BR) {
+    const long long i = (long long)row * SR + t;
+    y[i] = (yin ? yin[i] : 0.0) + acc;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_acheb4_cta(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                    const double* __restrict__ val, const double* __restrict__ dinv,
+                                                    const double* __restrict__ d, double* __restrict__ r,
+                                                    double* __restrict__ x, double* __restrict__ dout, double c1,
+                                                    double c2, int first, int want_r, int want_d) {
+  __shared__ double sh[8][4];
+  const int row = blockIdx.x, t = threadIdx.x;
+  const long long i = (long long)row * 4 + t;
+  const double acc = want_r ? cta_row<4, 4>(row, rp, ci, val, d, sh) : 0.0;
+  if (t >= 4) return;  // threads 0..3 own the row (lanes 0..3 of warp 0)
+  const double dv = d[i];
+  const double xv = first ? 0.0 : x[i];
+  x[i] = xv + dv;
+  if (!want_r) return;
+  const double rv = r[i] - acc;
+  r[i] = rv;
+  if (!want_d) return;
+  double D[4];
+  load_row<4>(dinv + (long long)row * 16 + t * 4, D);
+  double z = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) z += D[k] * __shfl_sync(0xfu, rv, k, 4);
+  dout[i] = c1 * dv + c2 * z;
+}
+
+__global__ void __launch_bounds__(256) k_aresid4_cta(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                     const double* __restrict__ val, const double* __restrict__ dinv,
+                                                     const double* __restrict__ b, const double* __restrict__ x,
+                                                     double* __restrict__ r, double* __restrict__ d, double c2) {
+  __shared__ double sh[8][4];
+  const int row = blockIdx.x, t = threadIdx.x;
+  const long long i = (long long)row * 4 + t;
+  const double acc = x ? cta_row<4, 4>(row, rp, ci, val, x, sh) : 0.0;
+  if (t >= 4) return;
+  const double rv = b[i] - acc;
+  r[i] = rv;
+  double D[4];
+  load_row<4>(dinv + (long long)row * 16 + t * 4, D);
+  double z = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) z += D[k] * __shfl_sync(0xfu, rv, k, 4);
+  d[i] = c2 * z;
+}
+
+// CTA-per-row form for levels whose rows are long (measured: small coarse levels were paced by
+// ~7 sequential dependent-load rounds per row at 32 lanes per row)
+static bool use_cta_rows(long long nnzb, int nb) { return nb > 0 && (double)nnzb / nb >= 48.0; }
+
 // slots (blocks in flight per block row) for the row-component kernels
 static int pick_slots(long long nnzb, int nb, int BR) {
   static const int shift = getenv("SEAICE_SLOT_SHIFT") ? atoi(getenv("SEAICE_SLOT_SHIFT")) : 0;  // tuning aid
@@ -1777,7 +1883,11 @@ static void gspmv(Ctx& c, int nb, int br, int bc, long long nnzb, const int* rp,
   } else if (br == 4 || bc == 4) {
     // b = 4 hierarchies (reading G30): row-major blocks, row-component lanes (val is AoS here)
     const int Sl = pick_slots(nnzb, nb, br);
-    if (br == 4 && bc == 4) {
+    if (use_cta_rows(nnzb, nb)) {
+      if (br == 4 && bc == 4) k_aspmv_cta<4, 4><<<nb, 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y);
+      else if (br == 2) k_aspmv_cta<2, 4><<<nb, 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y);
+      else k_aspmv_cta<4, 2><<<nb, 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y);
+    } else if (br == 4 && bc == 4) {
       SI_SDISPATCH(Sl, (k_aspmv<4, 4, SS><<<agrid(nb, 4 * SS), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
     } else if (br == 2) {
       SI_SDISPATCH(Sl, (k_aspmv<2, 4, SS><<<agrid(nb, 2 * SS), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
@@ -2116,6 +2226,28 @@ void amg_setup_impl(Ctx& c) {
   tick(c, "finish", c.nlev - 1);
 }
 
+// Lagged hierarchy (reading G31): the coarse levels of the last setup stay; the finest level's
+// block-diagonal inverse and lambda_max are recomputed from the current stencil J (the finest
+// smoother and residual read J itself), and the V-cycle graph is re-captured (its Chebyshev
+// coefficients depend on lambda_max).
+void amg_refresh_finest(Ctx& c) {
+  SI_CHECK(c.assembled && c.nlev > 1, SEAICE_ESTATE, "amg_refresh_finest without a multilevel hierarchy");
+  vgraph_destroy(c);
+  Level& L0 = c.lv[0];
+  k_stencil_to_bsr<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L0.rp.get(), L0.val.get());
+  SI_LAUNCHED(c);
+  SI_CUDA(cudaMemsetAsync(c.flag.get(), 0, sizeof(int) * 4, c.s));
+  {
+    Scratch S(c);
+    double* dnorm = S.get<double>(L0.nb);
+    level_diag<2>(c, L0, S, dnorm);
+  }
+  L0.lmax = power_lambda<2>(c, L0, 0);
+  const int flag = read_scalar(c, c.flag.get());
+  SI_CHECK(!(flag & 4), SEAICE_ENONFINITE, "AMG: singular diagonal block");
+  c.amg_ready = true;
+}
+
 // ------------------------------------------------------------------ host: V-cycle
 struct ChebCoef {
   double th, de, sg;
@@ -2162,7 +2294,10 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
         SI_GDISPATCH(G, (k_gresid<3, GG><<<ggrid(L.nb, GG), 256, 0, c.s>>>(
                             L.nb, L.rp.get(), L.ci.get(), L.valT.get(), L.dinv.get(), b, pre ? nullptr : x, r, d,
                             1.0 / k.th)))
-      else {
+      else if (use_cta_rows(L.nnzb, L.nb)) {
+        k_aresid4_cta<<<L.nb, 256, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), b,
+                                             pre ? nullptr : x, r, d, 1.0 / k.th);
+      } else {
         const int Sl = pick_slots(L.nnzb, L.nb, 4);
         SI_SDISPATCH(Sl, (k_aresid4<SS><<<agrid(L.nb, 4 * SS), 256, 0, c.s>>>(
                              L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), b, pre ? nullptr : x, r, d,
@@ -2216,7 +2351,10 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
         SI_GDISPATCH(G, (k_gcheb<3, GG><<<ggrid(L.nb, GG), 256, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.valT.get(),
                                                                          L.dinv.get(), d, r, x, d2, c1, c2, first,
                                                                          want_r, want_d)))
-      else {
+      else if (use_cta_rows(L.nnzb, L.nb)) {
+        k_acheb4_cta<<<L.nb, 256, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), d, r, x, d2,
+                                            c1, c2, first, want_r, want_d);
+      } else {
         const int Sl = pick_slots(L.nnzb, L.nb, 4);
         // late own-entry loads: measured 2357 -> 1555 us of coarse smoothing per V-cycle (config 4)
         SI_SDISPATCH(Sl, (k_acheb4<SS, true><<<agrid(L.nb, 4 * SS), 256, 0, c.s>>>(

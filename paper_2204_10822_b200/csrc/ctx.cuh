@@ -126,6 +126,8 @@ struct Ctx {
   Phys ph{};
   std::string err;
   long long launches = 0;
+  bool lag_ok = false;       // a hierarchy of this time step exists (amg_lag, reading G31)
+  int last_krylov_its = 0;   // Krylov iterations of the previous Newton solve
   long long sg_hits[SEAICE_SPGEMM_PATHS] = {0, 0, 0, 0, 0};  // SpGEMM path counters (seaice_spgemm_path_hits)
 
   // per-step state
@@ -281,6 +283,7 @@ void precond_apply(Ctx& c, const double* r, double* z);
 
 // amg.cu
 void amg_setup_impl(Ctx& c);
+void amg_refresh_finest(Ctx& c);
 void amg_vcycle(Ctx& c, const double* r, double* z);
 void amg_free(Ctx& c);
 

@@ -16,6 +16,10 @@ PRM = wl.PhysParams()
 
 def make_ctx(n, **kw):
     from paper_2204_10822_b200.seaice import SeaIce
+    # exact-Newton comparisons against the direct-solve oracle use the fixed Krylov tolerance
+    # (reading G13); the Eisenstat-Walker product default (G29) is compared with the oracle's
+    # same rule where a test asks for krylov_forcing=1
+    kw.setdefault("krylov_forcing", 0)
     return SeaIce(n, **kw)
 
 
@@ -325,3 +329,30 @@ def test_problem1_parity(n):
     assert st["converged"] == 1, st
     assert abs(st["newton_iters"] - ho["newton_iters"]) <= 1, (st["newton_iters"], ho["newton_iters"])
     assert np.linalg.norm(np_(vg) - vo) <= 1e-8 * np.linalg.norm(vo)
+
+
+@pytest.mark.parametrize("n,lag", [(32, 0), (64, 10), (64, 4)])
+def test_newton_ew_lagged_hierarchy_matches_oracle(n, lag):
+    """Product defaults (Eisenstat-Walker forcing, reading G29) with the lagged hierarchy of
+    reading G31 (amg_lag): GPU and oracle tier B (same AMG definition, same forcing and
+    rebuild rules) agree on the Newton count (+-1), the Krylov total (+-10 %), the number of full
+    AMG setups (+-1) and the converged velocity (1e-8), over two moving-cyclone steps."""
+    cfg = wl.Config(f"lag{n}", n, 2, 2, True)
+    hA = wl.ice_fields(cfg)
+    ctx = make_ctx(n, krylov_forcing=1, amg_lag=lag)
+    vo_ = None
+    vg = torch.zeros(ctx.N, dtype=torch.float64, device="cuda")
+    for s in range(2):
+        inp = wl.step_inputs(cfg, s, v_prev=vo_, h_A=hA)
+        vo_, _, ho = newton.solve_step(inp, PRM, linsolve="amg_fgmres", forcing=1, amg_lag=lag)
+        vin = vg.clone()
+        vg, st = ctx.solve_step(inp.dt, inp.t_new, inp.h, inp.A, vin, inp.v_air, inp.v_ocean)
+        assert st["converged"] == 1 and ho["converged"], (s, st)
+        assert abs(st["newton_iters"] - ho["newton_iters"]) <= 1, (s, st["newton_iters"], ho["newton_iters"])
+        ko = sum(k["iters"] for k in ho["krylov"])
+        assert abs(st["krylov_iters_total"] - ko) <= 0.1 * ko + 2, (s, st["krylov_iters_total"], ko)
+        so = sum(ho["amg_rebuilt"])
+        assert abs(st["amg_setups"] - so) <= 1, (s, st["amg_setups"], so)
+        if lag == 0:
+            assert st["amg_setups"] == st["newton_iters"]
+        assert np.linalg.norm(np_(vg) - vo_) <= 1e-8 * np.linalg.norm(vo_), s

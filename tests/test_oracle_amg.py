@@ -199,3 +199,23 @@ def test_v_column_is_near_null_for_the_plastic_part_and_reproduced_by_ptent():
     Ac = H["levels"][1]["A"].toarray()
     assert Ac.shape[0] % 4 == 0
     assert np.linalg.eigvalsh(0.5 * (Ac + Ac.T)).min() > 0
+
+
+def test_refresh_finest_keeps_coarse_levels_and_symmetry():
+    """Reading G31: the lagged hierarchy replaces only the finest operator (and its D^-1,
+    lambda_max); the coarse levels are those of the old hierarchy, and the V-cycle stays
+    symmetric (so it remains a valid SPD preconditioner for the new J)."""
+    pb, J = _jacobian(24, seed=5)
+    _, J2 = _jacobian(24, seed=9)
+    v = wl.random_velocity(24, 6, amp=0.05)
+    H = amg.setup(J, pb, v=v, coarse_max_dof=60)
+    H2 = amg.refresh_finest(H, J2)
+    assert H2["levels"][0]["A"] is not H["levels"][0]["A"]
+    assert abs(H2["levels"][0]["A"] - J2).max() == 0
+    for l in range(1, len(H["levels"])):
+        assert H2["levels"][l] is H["levels"][l]
+    assert H2["levels"][0]["P"] is H["levels"][0]["P"]
+    rng = np.random.default_rng(1)
+    r1, r2 = rng.standard_normal(J.shape[0]), rng.standard_normal(J.shape[0])
+    z1, z2 = amg.vcycle(H2, r1), amg.vcycle(H2, r2)
+    assert abs(z1 @ r2 - r1 @ z2) <= 1e-10 * abs(z1 @ r2)

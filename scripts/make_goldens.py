@@ -71,10 +71,13 @@ def run_cfg3(out):
             "newton": h["newton_iters"], "converged": bool(h["converged"]), "relres": h["res"][-1] / h["res"][0],
             "krylov": [k["iters"] for k in h["krylov"]], "levels": [k.get("levels") for k in h["krylov"]],
             "alphas": h["alpha"], "res": h["res"], "seconds": round(time.time() - t0, 1),
-            "generator": "scripts/make_goldens.py cfg3 (calls oracle/ only)"}
+            "generator": "scripts/make_goldens.py cfg3 (calls oracle/ only)",
+            "v_storage": "cfg3_v.npz: v at 65536 DOFs drawn by numpy default_rng(12345) (sorted) + ||v||_2"}
     with open(os.path.join(out, "cfg3_step1.json"), "w") as f:
         json.dump(meta, f)
-    np.savez_compressed(os.path.join(out, "cfg3_v.npz"), v_step1=v)
+    idx = np.sort(np.random.default_rng(SAMPLE_SEED).choice(v.size, size=65536, replace=False))
+    np.savez_compressed(os.path.join(out, "cfg3_v.npz"), sample_idx=idx.astype(np.int64), v_sample=v[idx],
+                        v_norm=np.array([np.linalg.norm(v)]))
 
 
 if __name__ == "__main__":

@@ -67,7 +67,8 @@ def test_cfg2_all_24_steps_match_oracle():
 
 def test_cfg3_step1_matches_oracle_tier_b():
     meta = json.load(open(_load("cfg3_step1.json")))
-    ref = np.load(_load("cfg3_v.npz"))["v_step1"]
+    gold = np.load(_load("cfg3_v.npz"))
+    idx, ref, ref_norm = gold["sample_idx"], gold["v_sample"], float(gold["v_norm"][0])
     from paper_2204_10822_b200.seaice import SeaIce
     cfg = wl.CONFIGS[3]
     inp = wl.step_inputs(cfg, 0)
@@ -76,8 +77,10 @@ def test_cfg3_step1_matches_oracle_tier_b():
     v, st = ctx.solve_step(inp.dt, inp.t_new, inp.h, inp.A, inp.v_prev, inp.v_air, inp.v_ocean)
     assert st["converged"] == 1, st
     assert abs(st["newton_iters"] - meta["newton"]) <= 1, (st["newton_iters"], meta["newton"])
-    err = np.linalg.norm(v.cpu().numpy() - ref) / np.linalg.norm(ref)
+    vg = v.cpu().numpy()
+    err = np.linalg.norm(vg[idx] - ref) / np.linalg.norm(ref)       # sampled relative L2
     assert err <= 1e-8, err
+    assert abs(np.linalg.norm(vg) - ref_norm) <= 1e-8 * ref_norm  # full-vector norm
     # FGMRES count per solve against the same AMG definition (the Newton paths coincide while
     # the iterates agree; compare the solves both sides performed)
     v0 = torch.zeros_like(v)

@@ -1656,121 +1656,12 @@ __global__ void __launch_bounds__(256) k_aspmv(int nb, const int* __restrict__ r
   if (own) y[i] = (yin ? yin[i] : 0.0) + acc;
 }
 
-// ------------------------------------------------------------------ symmetric b = 4 level storage
-// The Galerkin operators are symmetric (A_c = P^T A P with A symmetric); the V-cycle kernels of
-// b = 4 levels read only the upper triangle (diagonal included) plus, per row, the positions of
-// the transposed lower blocks inside it: block (i, j), j < i, is read as the transpose of the
-// stored block (j, i) of row j, which the GPU processed shortly before (rows are aggregates in
-// node order: row j is at most a few thousand rows back), so it is served from L2 and the DRAM
-// traffic for the values halves.  The full block rows stay in Level::val for the setup and the
-// seaice_amg_level view.
-struct Sym4 {
-  const int* urp;
-  const int* uci;
-  const double* uval;  // upper blocks (j >= i), row-major 4 x 4
-  const int* lrp;
-  const int* lci;      // lower columns j < i
-  const int* lpos;     // index of block (j, i) in uval
-};
-
-// lane a of a 4-lane block group: row a of the upper block (one 32-B load), column a of the
-// transposed lower block (four 8-B loads; the group's four lanes read the block's 128 B together)
-template <int S>
-__device__ __forceinline__ double grpS_row(int row, int nb, int lig, const Sym4& m, const double* __restrict__ x) {
-  constexpr int G = 4 * S;
-  const int a = lig & 3, slot = lig >> 2;
-  double acc = 0.0;
-  if (row < nb) {
-    {
-      const int e1 = __ldg(m.urp + row + 1);
-      int e = __ldg(m.urp + row) + slot;
-      for (; e + S < e1; e += 2 * S) {
-        const int c0 = __ldg(m.uci + e), c1 = __ldg(m.uci + e + S);
-        double v0[4], v1[4], x0[4], x1[4];
-        load_row<4>(m.uval + (long long)e * 16 + a * 4, v0);
-        load_row<4>(m.uval + (long long)(e + S) * 16 + a * 4, v1);
-        load_xblk<4>(x, c0, x0);
-        load_xblk<4>(x, c1, x1);
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc += v0[b] * x0[b] + v1[b] * x1[b];
-      }
-      if (e < e1) {
-        double v0[4], x0[4];
-        load_row<4>(m.uval + (long long)e * 16 + a * 4, v0);
-        load_xblk<4>(x, __ldg(m.uci + e), x0);
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc += v0[b] * x0[b];
-      }
-    }
-    {
-      const int e1 = __ldg(m.lrp + row + 1);
-      for (int e = __ldg(m.lrp + row) + slot; e < e1; e += S) {
-        const double* blk = m.uval + (long long)__ldg(m.lpos + e) * 16 + a;
-        double x0[4];
-        load_xblk<4>(x, __ldg(m.lci + e), x0);
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc += __ldg(blk + 4 * b) * x0[b];
-      }
-    }
-  }
-#pragma unroll
-  for (int off = 4; off < G; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
-  return acc;
-}
-
-__global__ void k_sym_count(int nb, const int* __restrict__ rp, const int* __restrict__ ci, int* __restrict__ ucnt,
-                            int* __restrict__ lcnt) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= nb) return;
-  int u = 0, l = 0;
-  for (int e = rp[r]; e < rp[r + 1]; ++e) (ci[e] >= r ? u : l)++;
-  ucnt[r] = u;
-  lcnt[r] = l;
-}
-__global__ void k_sym_fill(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
-                           const double* __restrict__ val, const int* __restrict__ urp, int* __restrict__ uci,
-                           double* __restrict__ uval, const int* __restrict__ lrp, int* __restrict__ lci) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= nb) return;
-  int u = urp[r], l = lrp[r];
-  for (int e = rp[r]; e < rp[r + 1]; ++e) {
-    const int col = ci[e];
-    if (col >= r) {
-      uci[u] = col;
-#pragma unroll
-      for (int t = 0; t < 16; ++t) uval[(long long)u * 16 + t] = val[(long long)e * 16 + t];
-      ++u;
-    } else {
-      lci[l++] = col;
-    }
-  }
-}
-__global__ void k_sym_lpos(int nb, const int* __restrict__ lrp, const int* __restrict__ lci,
-                           const int* __restrict__ urp, const int* __restrict__ uci, int* __restrict__ lpos,
-                           int* __restrict__ flag) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= nb) return;
-  for (int e = lrp[r]; e < lrp[r + 1]; ++e) {
-    const int j = lci[e];
-    int lo = urp[j], hi = urp[j + 1];
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (uci[mid] < r) lo = mid + 1;
-      else hi = mid;
-    }
-    if (lo < urp[j + 1] && uci[lo] == r) lpos[e] = lo;
-    else {
-      lpos[e] = urp[j];
-      atomicOr(flag, 16);  // structurally unsymmetric (cannot happen for a Galerkin product)
-    }
-  }
-}
-
 // Chebyshev step on a b = 4 level (semantics of k_gcheb).  LATE: the row's own vector entries
 // and D^-1 block are loaded after the SpMV (fewer live registers during the gather loop, at
 // the cost of one more round trip); otherwise before it.
 template <int S, bool LATE>
-__global__ void __launch_bounds__(256) k_acheb4(int nb, Sym4 m, const double* __restrict__ dinv,
+__global__ void __launch_bounds__(256) k_acheb4(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                const double* __restrict__ val, const double* __restrict__ dinv,
                                                 const double* __restrict__ d, double* __restrict__ r,
                                                 double* __restrict__ x, double* __restrict__ dout, double c1,
                                                 double c2, int first, int want_r, int want_d) {
@@ -1787,7 +1678,7 @@ __global__ void __launch_bounds__(256) k_acheb4(int nb, Sym4 m, const double* __
     if (want_d) load_row<4>(dinv + (long long)row * 16 + lig * 4, D);
   }
   double acc = 0.0;
-  if (want_r) acc = grpS_row<S>(row, nb, lig, m, d);
+  if (want_r) acc = grpA_row<4, 4, S>(row, nb, lig, rp, ci, val, d);
   if (LATE && own) {
     dv = d[i];
     if (!first) xv = x[i];
@@ -1807,7 +1698,8 @@ __global__ void __launch_bounds__(256) k_acheb4(int nb, Sym4 m, const double* __
 
 // r = b - A x (x may be NULL: r = b); d = c2 Dinv r on a b = 4 level
 template <int S>
-__global__ void __launch_bounds__(256) k_aresid4(int nb, Sym4 m, const double* __restrict__ dinv,
+__global__ void __launch_bounds__(256) k_aresid4(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                 const double* __restrict__ val, const double* __restrict__ dinv,
                                                  const double* __restrict__ b, const double* __restrict__ x,
                                                  double* __restrict__ r, double* __restrict__ d, double c2) {
   constexpr int G = 4 * S;
@@ -1816,7 +1708,7 @@ __global__ void __launch_bounds__(256) k_aresid4(int nb, Sym4 m, const double* _
   const bool own = row < nb && lig < 4;
   const long long i = (long long)row * 4 + lig;
   double bo = 0.0, D[4] = {0.0, 0.0, 0.0, 0.0};
-  const double acc = x ? grpS_row<S>(row, nb, lig, m, x) : 0.0;
+  const double acc = x ? grpA_row<4, 4, S>(row, nb, lig, rp, ci, val, x) : 0.0;
   if (own) {  // after the gather (fewer live registers in the loop, as k_acheb4)
     bo = b[i];
     load_row<4>(dinv + (long long)row * 16 + lig * 4, D);
@@ -1873,43 +1765,6 @@ __device__ __forceinline__ double cta_row(int row, const int* __restrict__ rp, c
   return tot;
 }
 
-// CTA-per-row gather on the symmetric storage (b = 4 levels)
-__device__ __forceinline__ double ctaS_row(int row, const Sym4& m, const double* __restrict__ x, double (*sh)[4]) {
-  constexpr int S = 64;
-  const int t = threadIdx.x, a = t & 3, slot = t >> 2;
-  double acc = 0.0;
-  {
-    const int e1 = __ldg(m.urp + row + 1);
-    for (int e = __ldg(m.urp + row) + slot; e < e1; e += S) {
-      double v0[4], x0[4];
-      load_row<4>(m.uval + (long long)e * 16 + a * 4, v0);
-      load_xblk<4>(x, __ldg(m.uci + e), x0);
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc += v0[b] * x0[b];
-    }
-  }
-  {
-    const int e1 = __ldg(m.lrp + row + 1);
-    for (int e = __ldg(m.lrp + row) + slot; e < e1; e += S) {
-      const double* blk = m.uval + (long long)__ldg(m.lpos + e) * 16 + a;
-      double x0[4];
-      load_xblk<4>(x, __ldg(m.lci + e), x0);
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc += __ldg(blk + 4 * b) * x0[b];
-    }
-  }
-#pragma unroll
-  for (int off = 4; off < 32; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if ((t & 31) < 4) sh[t >> 5][a] = acc;
-  __syncthreads();
-  double tot = 0.0;
-  if (t < 4) {
-#pragma unroll
-    for (int w = 0; w < 8; ++w) tot += sh[w][t];
-  }
-  return tot;
-}
-
 template <int BR, int BC>
 __global__ void __launch_bounds__(256) k_aspmv_cta(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
                                                    const double* __restrict__ val, const double* __restrict__ x,
@@ -1924,14 +1779,15 @@ __global__ void __launch_bounds__(256) k_aspmv_cta(int nb, const int* __restrict
   }
 }
 
-__global__ void __launch_bounds__(256) k_acheb4_cta(int nb, Sym4 m, const double* __restrict__ dinv,
+__global__ void __launch_bounds__(256) k_acheb4_cta(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                    const double* __restrict__ val, const double* __restrict__ dinv,
                                                     const double* __restrict__ d, double* __restrict__ r,
                                                     double* __restrict__ x, double* __restrict__ dout, double c1,
                                                     double c2, int first, int want_r, int want_d) {
   __shared__ double sh[8][4];
   const int row = blockIdx.x, t = threadIdx.x;
   const long long i = (long long)row * 4 + t;
-  const double acc = want_r ? ctaS_row(row, m, d, sh) : 0.0;
+  const double acc = want_r ? cta_row<4, 4>(row, rp, ci, val, d, sh) : 0.0;
   if (t >= 4) return;  // threads 0..3 own the row (lanes 0..3 of warp 0)
   const double dv = d[i];
   const double xv = first ? 0.0 : x[i];
@@ -1948,13 +1804,14 @@ __global__ void __launch_bounds__(256) k_acheb4_cta(int nb, Sym4 m, const double
   dout[i] = c1 * dv + c2 * z;
 }
 
-__global__ void __launch_bounds__(256) k_aresid4_cta(int nb, Sym4 m, const double* __restrict__ dinv,
+__global__ void __launch_bounds__(256) k_aresid4_cta(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                     const double* __restrict__ val, const double* __restrict__ dinv,
                                                      const double* __restrict__ b, const double* __restrict__ x,
                                                      double* __restrict__ r, double* __restrict__ d, double c2) {
   __shared__ double sh[8][4];
   const int row = blockIdx.x, t = threadIdx.x;
   const long long i = (long long)row * 4 + t;
-  const double acc = x ? ctaS_row(row, m, x, sh) : 0.0;
+  const double acc = x ? cta_row<4, 4>(row, rp, ci, val, x, sh) : 0.0;
   if (t >= 4) return;
   const double rv = b[i] - acc;
   r[i] = rv;
@@ -2044,37 +1901,6 @@ static void gspmv(Ctx& c, int nb, int br, int bc, long long nnzb, const int* rp,
 }
 
 // ------------------------------------------------------------------ host: setup
-static Sym4 sym4(Level& L) {
-  return Sym4{L.surp.get(), L.suci.get(), L.suval.get(), L.slrp.get(), L.slci.get(), L.slpos.get()};
-}
-
-// upper triangle + transposed-lower index of a b = 4 level (see Sym4)
-static void build_sym4(Ctx& c, Level& L) {
-  Scratch S(c);
-  const int nb = L.nb;
-  int* uc = S.get<int>(nb + 1);
-  int* lc = S.get<int>(nb + 1);
-  k_sym_count<<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.rp.get(), L.ci.get(), uc, lc);
-  SI_LAUNCHED(c);
-  SI_CUDA(cudaMemsetAsync(uc + nb, 0, sizeof(int), c.s));
-  SI_CUDA(cudaMemsetAsync(lc + nb, 0, sizeof(int), c.s));
-  L.surp.ensure(c.al, nb + 1);
-  L.slrp.ensure(c.al, nb + 1);
-  exclusive_scan(c, uc, L.surp.get(), nb + 1);
-  exclusive_scan(c, lc, L.slrp.get(), nb + 1);
-  const int nu = read_scalar(c, L.surp.get() + nb), nl = read_scalar(c, L.slrp.get() + nb);
-  L.suci.ensure(c.al, nu);
-  L.suval.ensure(c.al, (size_t)nu * 16);
-  L.slci.ensure(c.al, nl);
-  L.slpos.ensure(c.al, nl);
-  k_sym_fill<<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.rp.get(), L.ci.get(), L.val.get(), L.surp.get(), L.suci.get(),
-                                                 L.suval.get(), L.slrp.get(), L.slci.get());
-  k_sym_lpos<<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.slrp.get(), L.slci.get(), L.surp.get(), L.suci.get(),
-                                                 L.slpos.get(), c.flag.get());
-  SI_LAUNCHED(c);
-  c.launches += 1;
-}
-
 static BsrMat view(Level& L) { return BsrMat{L.nb, L.nb, L.b, L.b, L.nnzb, L.rp.get(), L.ci.get(), L.val.get()}; }
 
 template <int B>
@@ -2282,10 +2108,9 @@ void amg_free(Ctx& c) {
   c.vc_in.free_();
   c.vc_out.free_();
   for (auto& L : c.lv) {
-    DBuf<int>* ib[] = {&L.rp, &L.ci, &L.Prp, &L.Pci, &L.Rrp, &L.Rci, &L.agg, &L.surp, &L.suci, &L.slrp, &L.slci,
-                       &L.slpos};
+    DBuf<int>* ib[] = {&L.rp, &L.ci, &L.Prp, &L.Pci, &L.Rrp, &L.Rci, &L.agg};
     DBuf<double>* db[] = {&L.val, &L.dinv, &L.Pval, &L.Rval, &L.B, &L.x, &L.rhs, &L.r, &L.d, &L.d2, &L.z, &L.Tval,
-                          &L.suval, &L.valT, &L.PvalT, &L.RvalT};
+                          &L.valT, &L.PvalT, &L.RvalT};
     for (auto* b : ib) b->free_();
     for (auto* b : db) b->free_();
   }
@@ -2352,7 +2177,6 @@ void amg_setup_impl(Ctx& c) {
     else level_diag<4>(c, L, S, dnorm);
     tick(c, "diag", lvl);
     if (lvl > 0 && L.b != 4) tile_copy(c, L.valT, L.val.get(), L.nnzb, L.b * L.b);
-    if (lvl > 0 && L.b == 4) build_sym4(c, L);
     L.lmax = (L.b == 2) ? power_lambda<2>(c, L, lvl) : (L.b == 3) ? power_lambda<3>(c, L, lvl)
                                                                   : power_lambda<4>(c, L, lvl);
     tick(c, "power", lvl);
@@ -2398,7 +2222,6 @@ void amg_setup_impl(Ctx& c) {
   const int flag = read_scalar(c, c.flag.get());
   SI_CHECK(!(flag & 4), SEAICE_ENONFINITE, "AMG: singular diagonal block");
   SI_CHECK(!(flag & 8), SEAICE_ENONFINITE, "AMG: coarse matrix not positive definite");
-  SI_CHECK(!(flag & 16), SEAICE_ECUDA, "AMG: coarse operator not structurally symmetric");
   c.op_complexity = (double)nnz_total / (double)nnz0;
   c.amg_ready = true;
   tick(c, "finish", c.nlev - 1);
@@ -2473,12 +2296,12 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
                             L.nb, L.rp.get(), L.ci.get(), L.valT.get(), L.dinv.get(), b, pre ? nullptr : x, r, d,
                             1.0 / k.th)))
       else if (use_cta_rows(L.nnzb, L.nb)) {
-        k_aresid4_cta<<<L.nb, 256, 0, c.s>>>(L.nb, sym4(L), L.dinv.get(), b,
+        k_aresid4_cta<<<L.nb, 256, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), b,
                                              pre ? nullptr : x, r, d, 1.0 / k.th);
       } else {
         const int Sl = pick_slots(L.nnzb, L.nb, 4);
         SI_SDISPATCH(Sl, (k_aresid4<SS><<<agrid(L.nb, 4 * SS), 256, 0, c.s>>>(
-                             L.nb, sym4(L), L.dinv.get(), b, pre ? nullptr : x, r, d,
+                             L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), b, pre ? nullptr : x, r, d,
                              1.0 / k.th)))
       }
     }
@@ -2530,13 +2353,13 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
                                                                          L.dinv.get(), d, r, x, d2, c1, c2, first,
                                                                          want_r, want_d)))
       else if (use_cta_rows(L.nnzb, L.nb)) {
-        k_acheb4_cta<<<L.nb, 256, 0, c.s>>>(L.nb, sym4(L), L.dinv.get(), d, r, x, d2,
+        k_acheb4_cta<<<L.nb, 256, 0, c.s>>>(L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), d, r, x, d2,
                                             c1, c2, first, want_r, want_d);
       } else {
         const int Sl = pick_slots(L.nnzb, L.nb, 4);
         // late own-entry loads: measured 2357 -> 1555 us of coarse smoothing per V-cycle (config 4)
         SI_SDISPATCH(Sl, (k_acheb4<SS, true><<<agrid(L.nb, 4 * SS), 256, 0, c.s>>>(
-                             L.nb, sym4(L), L.dinv.get(), d, r, x, d2, c1, c2, first,
+                             L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), d, r, x, d2, c1, c2, first,
                              want_r, want_d)))
       }
     }

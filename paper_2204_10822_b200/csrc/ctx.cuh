@@ -32,9 +32,6 @@ struct Level {
   // V-cycle copies of val / Pval / Rval in the chunk-of-32 SoA layout read by the group-per-row
   // kernels: element j of block e at ((e >> 5) * BB + j) * 32 + (e & 31)  (coalesced loads)
   DBuf<double> valT, PvalT, RvalT;
-  // b = 4 levels: upper triangle (incl. diagonal) + transposed-lower index (amg.cu Sym4)
-  DBuf<int> surp, suci, slrp, slci, slpos;
-  DBuf<double> suval;
 };
 
 // Grow-only chunked bump allocator for setup scratch (LIFO marks): avoids an allocator

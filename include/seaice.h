@@ -104,7 +104,8 @@ typedef struct {
   int32_t spgemm_path;     /* 0 (default): SpGEMM code path chosen by row-expansion size; testing knob
                               to force one path for every product: 1 hash tables (1k, else 4k
                               entries, else sort), 2 sort + thread-per-row numeric, 3 sort + 8-lane
-                              groups, 4 sort + warp per row (see seaice_spgemm_path_hits) */
+                              groups, 4 sort + warp per row, 5 8-lane hash tables (falls back when a
+                              row's expansion exceeds 256) (see seaice_spgemm_path_hits) */
   int32_t amg_lag;         /* 0: full AMG setup at every Newton iteration; T > 0 (reading G31):
                               at Newton iteration l >= 1 of a time step the hierarchy is rebuilt only
                               if the previous linear solve needed more than T Krylov iterations,
@@ -290,8 +291,11 @@ int seaice_profile_read(seaice_ctx* ctx, double* ms_host, int64_t* launches_host
  * counted since create (the numeric result is the same definition on every path;
  * the choice depends only on row-expansion sizes).  hits[0] 1k-entry hash table per row,
  * [1] 4k-entry hash table, [2] sort-based thread-per-row numeric, [3] sort-based 8-lane-group
- * numeric, [4] sort-based warp-per-row (wide rows).  n_host: entries to write (<= 5). */
-#define SEAICE_SPGEMM_PATHS 5
+ * numeric, [4] sort-based warp-per-row (wide rows), [5] 8-lane-per-row hash tables (short Y
+ * rows: the level-0 Galerkin products), [6] numeric phase by a CTA per row with shared-memory
+ * accumulators (levels of <= 16384 rows whose rows have <= 640 block columns; replaces the
+ * numeric kernel of paths 0, 1 and 4 there).  n_host: entries to write (<= 7). */
+#define SEAICE_SPGEMM_PATHS 7
 int seaice_spgemm_path_hits(const seaice_ctx* ctx, int64_t* hits_host, int32_t n_host);
 
 /* Bytes of device memory the context currently holds (and its peak). */

@@ -864,6 +864,181 @@ __global__ void __launch_bounds__(32 * HW) k_sg_hash_numeric(
   }
 }
 
+// ------------------------------------------------------------------ narrow-row hash SpGEMM
+// Same algorithm as the k_sg_hash_* kernels (per-row open-addressing table of column ids, sorted
+// row pattern, numeric accumulation in X-entry order, so values are bitwise identical to the other
+// paths), for products whose Y rows are short (level 0: R A with A's 9 blocks per row, (R A) P with
+// P's ~3): a group of kNG = 8 lanes owns one row (4 rows per warp) instead of a whole warp, so 3 or
+// 9 Y entries do not leave 29 or 23 of 32 lanes idle.  Table kNHT slots per row (expansion <=
+// kNHT / 2); the row pattern is ordered by a rank count (u <= kNHT / 2).
+constexpr int kNG = 8, kNHT = 512, kNW = 2;  // lanes per row, slots per row, warps per block
+constexpr int kNRows = (32 / kNG) * kNW;      // rows per block
+
+__device__ __forceinline__ unsigned grp_mask() {
+  return ((1u << kNG) - 1u) << ((threadIdx.x & 31) & ~(kNG - 1));
+}
+
+__global__ void __launch_bounds__(32 * kNW) k_sgn_count(int nr, const int* __restrict__ xrp, const int* __restrict__ xci,
+                                                         const int* __restrict__ yrp, const int* __restrict__ yci,
+                                                         int* __restrict__ cnt) {
+  __shared__ int tabs[kNRows][kNHT];
+  const int g = threadIdx.x / kNG, l = threadIdx.x % kNG;
+  const int r = blockIdx.x * kNRows + g;
+  const unsigned gm = grp_mask();
+  int* tab = tabs[g];
+  if (r > nr) return;  // uniform per group
+  if (r == nr) {
+    if (l == 0) cnt[r] = 0;
+    return;
+  }
+  for (int t = l; t < kNHT; t += kNG) tab[t] = -1;
+  __syncwarp(gm);
+  int u = 0;
+  for (int e = xrp[r]; e < xrp[r + 1]; ++e) {
+    const int j = xci[e];
+    for (int f = yrp[j] + l; f < yrp[j + 1]; f += kNG) u += hinsert<kNHT>(tab, yci[f]);
+  }
+#pragma unroll
+  for (int o = kNG / 2; o > 0; o >>= 1) u += __shfl_xor_sync(gm, u, o, kNG);
+  if (l == 0) cnt[r] = u;
+}
+
+__global__ void __launch_bounds__(32 * kNW) k_sgn_cols(int nr, const int* __restrict__ xrp, const int* __restrict__ xci,
+                                                        const int* __restrict__ yrp, const int* __restrict__ yci,
+                                                        const int* __restrict__ crp, int* __restrict__ cci) {
+  __shared__ int tabs[kNRows][kNHT];
+  const int g = threadIdx.x / kNG, l = threadIdx.x % kNG;
+  const int r = blockIdx.x * kNRows + g;
+  const unsigned gm = grp_mask();
+  if (r >= nr) return;
+  int* tab = tabs[g];
+  for (int t = l; t < kNHT; t += kNG) tab[t] = -1;
+  __syncwarp(gm);
+  for (int e = xrp[r]; e < xrp[r + 1]; ++e) {
+    const int j = xci[e];
+    for (int f = yrp[j] + l; f < yrp[j + 1]; f += kNG) hinsert<kNHT>(tab, yci[f]);
+  }
+  __syncwarp(gm);
+  // compact (slot order) into the table front
+  const int lane = threadIdx.x & 31;
+  const unsigned below = gm & ((1u << lane) - 1u);
+  int base = 0;
+  for (int t0 = 0; t0 < kNHT; t0 += kNG) {
+    const int k = tab[t0 + l];
+    const unsigned m = __ballot_sync(gm, k != -1);
+    __syncwarp(gm);
+    if (k != -1) tab[base + __popc(m & below)] = k;
+    base += __popc(m);
+    __syncwarp(gm);
+  }
+  // order by rank (keys are distinct)
+  const int u = crp[r + 1] - crp[r];
+  int* out = cci + crp[r];
+  for (int q = l; q < u; q += kNG) {
+    const int key = tab[q];
+    int rank = 0;
+    for (int t = 0; t < u; ++t) rank += tab[t] < key;
+    out[rank] = key;
+  }
+}
+
+template <int M, int K, int P>
+__global__ void __launch_bounds__(32 * kNW) k_sgn_numeric(int nr, const int* __restrict__ xrp,
+                                                           const int* __restrict__ xci, const double* __restrict__ xv,
+                                                           const int* __restrict__ yrp, const int* __restrict__ yci,
+                                                           const double* __restrict__ yv, const int* __restrict__ crp,
+                                                           const int* __restrict__ cci, double* __restrict__ cv) {
+  __shared__ int keys[kNRows][kNHT];
+  __shared__ int pos[kNRows][kNHT];
+  const int g = threadIdx.x / kNG, l = threadIdx.x % kNG;
+  const int r = blockIdx.x * kNRows + g;
+  const unsigned gm = grp_mask();
+  if (r >= nr) return;
+  int* kt = keys[g];
+  int* pt = pos[g];
+  for (int t = l; t < kNHT; t += kNG) kt[t] = -1;
+  __syncwarp(gm);
+  const int c0 = crp[r], c1 = crp[r + 1];
+  for (int q = c0 + l; q < c1; q += kNG) {
+    const int key = cci[q];
+    unsigned h = hslot<kNHT>(key);
+    while (atomicCAS(kt + h, -1, key) != -1) h = (h + 1) & (kNHT - 1);
+    pt[h] = q;
+  }
+  for (long long t = (long long)c0 * M * P + l; t < (long long)c1 * M * P; t += kNG) cv[t] = 0.0;
+  __syncwarp(gm);
+  for (int e = xrp[r]; e < xrp[r + 1]; ++e) {
+    const int j = xci[e];
+    double xb[M * K];
+#pragma unroll
+    for (int t = 0; t < M * K; ++t) xb[t] = xv[(long long)e * M * K + t];
+    for (int f = yrp[j] + l; f < yrp[j + 1]; f += kNG) {
+      const int col = yci[f];
+      unsigned h = hslot<kNHT>(col);
+      while (kt[h] != col) h = (h + 1) & (kNHT - 1);
+      double* cb = cv + (long long)pt[h] * M * P;
+      const double* yb = yv + (long long)f * K * P;
+#pragma unroll
+      for (int a = 0; a < M; ++a)
+#pragma unroll
+        for (int b = 0; b < P; ++b) {
+          double s = cb[a * P + b];
+#pragma unroll
+          for (int k = 0; k < K; ++k) s += xb[a * K + k] * yb[k * P + b];
+          cb[a * P + b] = s;
+        }
+    }
+    __syncwarp(gm);
+  }
+}
+
+// ------------------------------------------------------------------ CTA-per-row numeric (small levels)
+// On the small coarse levels a few hundred rows each expand to thousands of block products; one
+// warp per row (hash / sort paths) then runs them as a long serial chain of global
+// read-modify-writes (measured 3-5 ms per product on 32-160-row levels).  Here a CTA owns a row:
+// the row's sorted pattern and its accumulators live in shared memory, and for each X entry
+// (sequential, so every output entry still accumulates in X-entry order: values are bitwise
+// identical to the other paths) the 256 threads split the Y row's (entry, block element) pairs.
+constexpr int kCtaRows = 16384, kCtaMaxCols = 640;
+
+template <int M, int K, int P>
+__global__ void __launch_bounds__(256) k_sg_cta_numeric(int nr, const int* __restrict__ xrp,
+                                                        const int* __restrict__ xci, const double* __restrict__ xv,
+                                                        const int* __restrict__ yrp, const int* __restrict__ yci,
+                                                        const double* __restrict__ yv, const int* __restrict__ crp,
+                                                        const int* __restrict__ cci, double* __restrict__ cv) {
+  constexpr int MP = M * P;
+  extern __shared__ double sm[];
+  const int r = blockIdx.x;
+  const int c0 = crp[r], u = crp[r + 1] - c0;
+  double* acc = sm;
+  int* cols = reinterpret_cast<int*>(acc + (long long)u * MP);
+  for (int t = threadIdx.x; t < u; t += blockDim.x) cols[t] = cci[c0 + t];
+  for (int t = threadIdx.x; t < u * MP; t += blockDim.x) acc[t] = 0.0;
+  __syncthreads();
+  for (int e = xrp[r]; e < xrp[r + 1]; ++e) {
+    const int j = xci[e];
+    const double* xb = xv + (long long)e * M * K;
+    const int f0 = yrp[j], nf = yrp[j + 1] - f0;
+    for (int idx = threadIdx.x; idx < nf * MP; idx += blockDim.x) {
+      const int f = f0 + idx / MP, ent = idx % MP, a = ent / P, b = ent % P;
+      const int col = yci[f];
+      int lo = 0, hi = u;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cols[mid] < col) lo = mid + 1;
+        else hi = mid;
+      }
+      double sum = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) sum += __ldg(xb + a * K + k) * __ldg(yv + (long long)f * K * P + k * P + b);
+      acc[lo * MP + ent] += sum;
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < u * MP; t += blockDim.x) cv[(long long)c0 * MP + t] = acc[t];
+}
+
 struct BsrMat {
   int nbr = 0, nbc = 0, br = 0, bc = 0;
   long long nnzb = 0;
@@ -871,6 +1046,35 @@ struct BsrMat {
   int* ci = nullptr;
   double* val = nullptr;
 };
+
+// Small levels: CTA-per-row numeric if every row's pattern fits the shared accumulators.
+// Returns true if it ran (crp / cci / cval already sized, pattern written).
+template <int M, int K, int P>
+static bool cta_numeric(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBuf<int>& cci,
+                        DBuf<double>& cval, const int* cnt, Scratch& S) {
+  const int nr = X.nbr;
+  if (nr > kCtaRows || c.p.spgemm_path != 0) return false;
+  int* mx = S.get<int>(1);
+  size_t tmp = 0;
+  SI_CUDA(cub::DeviceReduce::Max(nullptr, tmp, cnt, mx, nr, c.s));
+  void* t = S.get<char>(tmp + 16);
+  SI_CUDA(cub::DeviceReduce::Max(t, tmp, cnt, mx, nr, c.s));
+  c.launches += 1;
+  const int umax = read_scalar(c, mx);
+  if (umax > kCtaMaxCols) return false;
+  const size_t smem = (size_t)umax * (M * P * sizeof(double) + sizeof(int)) + 16;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SI_CUDA(cudaFuncSetAttribute(k_sg_cta_numeric<M, K, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kCtaMaxCols * (M * P * (int)sizeof(double) + (int)sizeof(int)) + 16));
+    attr_set = true;
+  }
+  k_sg_cta_numeric<M, K, P><<<nr, 256, smem, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp.get(), cci.get(),
+                                                     cval.get());
+  SI_LAUNCHED(c);
+  c.sg_hits[6]++;
+  return true;
+}
 
 // hash path: every row's expansion fits the per-warp shared-memory table of HT slots
 template <int M, int K, int P, int HT, int HW>
@@ -889,10 +1093,34 @@ static void hash_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp
   cval.ensure(c.al, cnnzb * M * P);
   k_sg_hash_cols<HT, HW><<<hb, 32 * HW, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, crp.get(), cci.get());
   SI_LAUNCHED(c);
-  k_sg_hash_numeric<M, K, P, HT, HW><<<hb, 32 * HW, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val,
-                                                               crp.get(), cci.get(), cval.get());
-  SI_LAUNCHED(c);
+  if (!cta_numeric<M, K, P>(c, X, Y, crp, cci, cval, cnt, S)) {
+    k_sg_hash_numeric<M, K, P, HT, HW><<<hb, 32 * HW, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val,
+                                                                 crp.get(), cci.get(), cval.get());
+    SI_LAUNCHED(c);
+  }
   tick(c, HT == kHT ? "  sg.hash1k" : "  sg.hash4k", nr);
+}
+
+template <int M, int K, int P>
+static void narrow_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBuf<int>& cci,
+                          DBuf<double>& cval, long long& cnnzb, Scratch& S) {
+  const int nr = X.nbr;
+  const int hb = (nr + 1 + kNRows - 1) / kNRows;
+  int* cnt = S.get<int>(nr + 1);
+  k_sgn_count<<<hb, 32 * kNW, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, cnt);
+  SI_LAUNCHED(c);
+  crp.ensure(c.al, nr + 1);
+  exclusive_scan(c, cnt, crp.get(), nr + 1);
+  cnnzb = read_scalar(c, crp.get() + nr);
+  SI_CHECK(cnnzb < (1LL << 31), SEAICE_EINVAL, "SpGEMM result exceeds int32 indexing");
+  cci.ensure(c.al, cnnzb);
+  cval.ensure(c.al, cnnzb * M * P);
+  k_sgn_cols<<<hb, 32 * kNW, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, crp.get(), cci.get());
+  SI_LAUNCHED(c);
+  k_sgn_numeric<M, K, P><<<hb, 32 * kNW, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp.get(), cci.get(),
+                                                    cval.get());
+  SI_LAUNCHED(c);
+  tick(c, "  sg.narrow", nr);
 }
 
 // Output arrays are grow-only DBufs owned by the caller.
@@ -918,6 +1146,12 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
     // the per-warp table has a fixed per-row cost: short rows (finest level) stay on the
     // sort-based path, whose thread-per-row numeric phase suits them
     const int force = c.p.spgemm_path;  // testing knob (seaice_params.spgemm_path)
+    const double ylen = Y.nbr > 0 ? (double)Y.nnzb / Y.nbr : 1.0;
+    if ((force == 5 || (force == 0 && ylen <= 12.0 && tot >= 24LL * nr)) && maxub <= kNHT / 2) {
+      c.sg_hits[5]++;
+      narrow_spgemm<M, K, P>(c, X, Y, crp, cci, cval, cnnzb, S);
+      return;
+    }
     const bool wide_rows = force == 1 || (force == 0 && tot >= 32LL * nr);
     if (wide_rows && maxub <= kHT / 2) {
       c.sg_hits[0]++;
@@ -971,8 +1205,9 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
   if (wide) {
     k_spgemm_compact_w<<<wgrid(nr), 256, 0, c.s>>>(nr, off, k1, crp.get(), cci.get());
     SI_LAUNCHED(c);
-    k_spgemm_numeric_w<M, K, P><<<wgrid(nr), 256, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp.get(),
-                                                            cci.get(), cval.get());
+    if (!cta_numeric<M, K, P>(c, X, Y, crp, cci, cval, cnt, S))
+      k_spgemm_numeric_w<M, K, P><<<wgrid(nr), 256, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp.get(),
+                                                              cci.get(), cval.get());
   } else {
     k_spgemm_compact<<<grid_for(nr), kThreads, 0, c.s>>>(nr, off, k1, crp.get(), cci.get());
     SI_LAUNCHED(c);

@@ -72,7 +72,7 @@ void validate(const seaice_params* p) {
   SI_CHECK(p->krylov_forcing == 0 || p->krylov_forcing == 1, SEAICE_EINVAL, "krylov_forcing must be 0 or 1");
   SI_CHECK(p->nullspace_dim == 3 || p->nullspace_dim == 4, SEAICE_EINVAL, "nullspace_dim must be 3 or 4");
   SI_CHECK(p->krylov_method == 0 || p->krylov_method == 1, SEAICE_EINVAL, "krylov_method must be 0 or 1");
-  SI_CHECK(p->spgemm_path >= 0 && p->spgemm_path <= 4, SEAICE_EINVAL, "spgemm_path must be in 0..4");
+  SI_CHECK(p->spgemm_path >= 0 && p->spgemm_path <= 5, SEAICE_EINVAL, "spgemm_path must be in 0..5");
   SI_CHECK(p->amg_lag >= 0, SEAICE_EINVAL, "amg_lag must be >= 0");
 }
 

@@ -128,7 +128,7 @@ struct Ctx {
   long long launches = 0;
   bool lag_ok = false;       // a hierarchy of this time step exists (amg_lag, reading G31)
   int last_krylov_its = 0;   // Krylov iterations of the previous Newton solve
-  long long sg_hits[SEAICE_SPGEMM_PATHS] = {0, 0, 0, 0, 0};  // SpGEMM path counters (seaice_spgemm_path_hits)
+  long long sg_hits[SEAICE_SPGEMM_PATHS] = {0, 0, 0, 0, 0, 0, 0};  // SpGEMM path counters (seaice_spgemm_path_hits)
 
   // per-step state
   bool step_set = false, assembled = false, amg_ready = false;

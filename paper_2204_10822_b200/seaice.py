@@ -280,8 +280,8 @@ class SeaIce:
 
     def spgemm_path_hits(self):
         """Counts of the SpGEMM code paths taken since create (seaice_spgemm_path_hits)."""
-        h = (C.c_int64 * 5)()
-        self._check(self.L.seaice_spgemm_path_hits(self.h, h, 5))
+        h = (C.c_int64 * 7)()
+        self._check(self.L.seaice_spgemm_path_hits(self.h, h, 7))
         return list(h)
 
     def memory(self):

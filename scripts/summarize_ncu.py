@@ -15,6 +15,7 @@ G = os.path.join(ROOT, "gpurun_out")
 P = os.path.join(ROOT, "profiles")
 TAG = sys.argv[1] if len(sys.argv) > 1 else "r01"
 CLASS = [("k_chebM_stencil", "cheb0_fused"), ("k_cheb_stencil", "cheb0"), ("k_gcheb", "cheb_coarse"),
+         ("k_acheb4", "cheb_coarse"), ("k_aresid4", "resid_coarse"), ("k_aspmv", "transfer"),
          ("k_gresid", "resid_coarse"), ("k_gspmv", "transfer"), ("k_resid_dinv_stencil", "resid0"),
          ("k_dense_gemv", "coarse_solve"), ("k_stencil_spmv", "spmv0"), ("k_multidot", "multidot"),
          ("k_multi_axpy_norm", "maxpy_norm"), ("k_assemble_had", "assemble"), ("k_delta_energy", "delta_energy")]
@@ -122,5 +123,7 @@ for tag, cls in (("assemble", "assemble"),):
             tot += float(v) * conv[u]
         traffic[cls] = tot
 if traffic:
+    traffic["_source"] = (f"profiles/{TAG}_ncu_vcycle_launches.csv (one V-cycle, config 4 late iterate, warm "
+                          f"caches) and profiles/{TAG}_ncu_full_assemble.json; DRAM bytes per launch, class mean")
     json.dump(traffic, open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
-    print("traffic:", {k: round(v / 1e6, 1) for k, v in traffic.items()}, "MB/launch")
+    print("traffic:", {k: round(v / 1e6, 1) for k, v in traffic.items() if not k.startswith("_")}, "MB/launch")

@@ -247,7 +247,7 @@ def test_fused_chebyshev_matches_per_step(n):
 
 
 
-PATHS = ["hash1k", "hash4k", "sort_thread", "sort_group8", "sort_warp"]
+PATHS = ["hash1k", "hash4k", "sort_thread", "sort_group8", "sort_warp", "hash_narrow", "cta_numeric"]
 
 
 def _plastic_state(n, seed):
@@ -259,7 +259,7 @@ def _plastic_state(n, seed):
     return inp, pb, v, pb.pi_consistent(v)
 
 
-@pytest.mark.parametrize("n,path", [(256, 0), (512, 0), (256, 1), (256, 2), (256, 3), (256, 4)])
+@pytest.mark.parametrize("n,path", [(256, 0), (512, 0), (256, 1), (256, 2), (256, 3), (256, 4), (256, 5)])
 def test_hierarchy_matches_oracle_at_scale(n, path):
     """AMG hierarchy parity at sizes that take the SpGEMM code paths config 4 uses (verdict r1):
     same level count, identical aggregates, A_l and P_l to 1e-11 row-relative, with the automatic
@@ -294,7 +294,7 @@ def test_config4_spgemm_paths_are_parity_covered():
     """Runs after test_hierarchy_matches_oracle_at_scale (file order): the paths config 4's setup
     takes (a plastic state and a late Newton iterate of its first step) are all among those the
     n = 256 / 512 parity cases exercised."""
-    if len(_covered) < 6:
+    if len(_covered) < 7:
         pytest.skip("needs test_hierarchy_matches_oracle_at_scale in the same session")
     covered = set().union(*_covered.values())
     cfg = wl.CONFIGS[4]

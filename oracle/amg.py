@@ -248,13 +248,16 @@ def setup(J, pb=None, theta=0.04, coarse_max_dof=400, max_levels=25, power_iters
           cheb_degree=3, cheb_lower=0.03, cheb_upper=1.1, n=None, L=512e3, agg_dist0=2, agg_dist=2,
           v=None, nullspace_dim=4):
     """nullspace_dim = 4 (reading G30) appends the linearisation point v (required then) to
-    the three rigid-body modes; coarse levels then carry 4 x 4 blocks."""
+    the three rigid-body modes; coarse levels then carry 4 x 4 blocks.  If v is identically
+    zero the three rigid-body modes are used (3 x 3 coarse blocks)."""
     if pb is not None:
         n, L = pb.n, pb.L
     A = J.tocsr()
     b = 2
     if nullspace_dim == 4 and v is None:
         raise ValueError("nullspace_dim = 4 needs the linearisation point v")
+    if nullspace_dim == 4 and not np.any(v):
+        nullspace_dim = 3  # reading G30: v_l = 0 (e.g. the first iterate from rest) adds no column
     B = level0_nullspace(n, L, v if nullspace_dim == 4 else None)
     K = B.shape[1]
     levels = []

@@ -1299,6 +1299,107 @@ __global__ void k_smooth_p(int nb, const int* __restrict__ trp, const int* __res
   }
 }
 
+// Level 0: P = P_tent - omega D^-1 (A P_tent) in one pass.  P_tent has one block per aggregated
+// node (Q_j in column agg(j)), so row i of A P_tent gathers A_ij Q_j over i's stencil neighbours,
+// grouped by agg(j): the row pattern is the sorted set of neighbour aggregates.  Same arithmetic
+// and order as the generic SpGEMM (A entries in row order) followed by k_smooth_p.  Rows hold at
+// most kPtsmMax A blocks (the finest stencil: 9).
+constexpr int kPtsmMax = 16;
+
+__device__ __forceinline__ int ptsm_cols(int i, const int* __restrict__ rp, const int* __restrict__ ci,
+                                         const int* __restrict__ agg, int (&ag)[kPtsmMax], int (&cols)[kPtsmMax],
+                                         int& ne) {
+  const int e0 = rp[i];
+  ne = rp[i + 1] - e0;
+  int u = 0;
+#pragma unroll
+  for (int t = 0; t < kPtsmMax; ++t) {
+    ag[t] = (t < ne) ? agg[ci[e0 + t]] : -1;
+    if (ag[t] >= 0) {  // insertion into the sorted distinct list
+      int p = u;
+      bool dup = false;
+      for (int q = 0; q < u; ++q) dup |= (cols[q] == ag[t]);
+      if (!dup) {
+        while (p > 0 && cols[p - 1] > ag[t]) {
+          cols[p] = cols[p - 1];
+          --p;
+        }
+        cols[p] = ag[t];
+        ++u;
+      }
+    }
+  }
+  return u;
+}
+
+__global__ void k_ptsm_count(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                             const int* __restrict__ agg, int* __restrict__ cnt, int* __restrict__ flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > nb) return;
+  if (i == nb) {
+    cnt[i] = 0;
+    return;
+  }
+  if (rp[i + 1] - rp[i] > kPtsmMax) {
+    atomicOr(flag, 32);
+    cnt[i] = 0;
+    return;
+  }
+  int ag[kPtsmMax], cols[kPtsmMax], ne;
+  cnt[i] = ptsm_cols(i, rp, ci, agg, ag, cols, ne);
+}
+
+template <int B, int K>
+__global__ void k_ptsm_fill(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ av, const int* __restrict__ agg,
+                            const int* __restrict__ ptrp, const double* __restrict__ ptval,
+                            const double* __restrict__ dinv, double omega, const int* __restrict__ prp,
+                            int* __restrict__ pci, double* __restrict__ pval) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nb) return;
+  int ag[kPtsmMax], cols[kPtsmMax], ne;
+  const int u = ptsm_cols(i, rp, ci, agg, ag, cols, ne);
+  const int e0 = rp[i], o = prp[i];
+  const int ai = agg[i];
+  const double* D = dinv + (long long)i * B * B;
+  for (int s = 0; s < u; ++s) {
+    const int J = cols[s];
+    double T[B * K];
+#pragma unroll
+    for (int t = 0; t < B * K; ++t) T[t] = 0.0;
+#pragma unroll
+    for (int t = 0; t < kPtsmMax; ++t) {
+      if (t < ne && ag[t] == J) {
+        const int j = ci[e0 + t];
+        const double* a = av + (long long)(e0 + t) * B * B;
+        const double* q = ptval + (long long)ptrp[j] * B * K;
+#pragma unroll
+        for (int r = 0; r < B; ++r)
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            double sum = T[r * K + k];
+#pragma unroll
+            for (int b = 0; b < B; ++b) sum += a[r * B + b] * q[b * K + k];
+            T[r * K + k] = sum;
+          }
+      }
+    }
+    pci[o + s] = J;
+    double* Pv = pval + (long long)(o + s) * B * K;
+#pragma unroll
+    for (int a = 0; a < B; ++a)
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double sm = 0.0;
+#pragma unroll
+        for (int b = 0; b < B; ++b) sm += D[a * B + b] * T[b * K + k];
+        double v = -omega * sm;
+        if (J == ai) v += ptval[(long long)ptrp[i] * B * K + a * K + k];
+        Pv[a * K + k] = v;
+      }
+  }
+}
+
 template <int K>
 __global__ void k_fix_zero_diag(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
                                 double* __restrict__ val) {
@@ -2278,15 +2379,38 @@ static void build_transfer(Ctx& c, Level& L, Level& Lc, int lvl, int na, Scratch
   tick(c, "tentative", lvl);
   BsrMat Pt{nb, na, B, K, ptn, ptrp, ptci, ptval};
   // T = A P_tent ; P = P_tent - omega Dinv T  (P takes T's pattern)
-  long long tn = 0;
-  spgemm<B, B, K>(c, view(L), Pt, L.Prp, L.Pci, L.Tval, tn);
-  tick(c, "A*Pt", lvl);
-  L.Pnnzb = tn;
-  L.Pval.ensure(c.al, (size_t)tn * B * K);
   const double omega = 4.0 / (3.0 * L.lmax);
-  k_smooth_p<B, K><<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.Prp.get(), L.Pci.get(), L.Tval.get(), L.dinv.get(),
-                                                    L.agg.get(), ptrp, ptval, omega, L.Pval.get());
-  SI_LAUNCHED(c);
+  bool fused = false;
+  if (B == 2 && c.p.spgemm_path == 0) {  // finest level: one-pass smoothed prolongator
+    int* cnt = S.get<int>(nb + 1);
+    SI_CUDA(cudaMemsetAsync(c.flag.get() + 2, 0, sizeof(int), c.s));
+    k_ptsm_count<<<grid_for(nb + 1), kThreads, 0, c.s>>>(nb, L.rp.get(), L.ci.get(), L.agg.get(), cnt,
+                                                        c.flag.get() + 2);
+    SI_LAUNCHED(c);
+    if (read_scalar(c, c.flag.get() + 2) == 0) {
+      L.Prp.ensure(c.al, nb + 1);
+      exclusive_scan(c, cnt, L.Prp.get(), nb + 1);
+      L.Pnnzb = read_scalar(c, L.Prp.get() + nb);
+      L.Pci.ensure(c.al, L.Pnnzb);
+      L.Pval.ensure(c.al, (size_t)L.Pnnzb * B * K);
+      k_ptsm_fill<B, K><<<grid_for(nb, 128), 128, 0, c.s>>>(nb, L.rp.get(), L.ci.get(), L.val.get(), L.agg.get(),
+                                                           ptrp, ptval, L.dinv.get(), omega, L.Prp.get(),
+                                                           L.Pci.get(), L.Pval.get());
+      SI_LAUNCHED(c);
+      fused = true;
+      tick(c, "A*Pt+smooth", lvl);
+    }
+  }
+  if (!fused) {
+    long long tn = 0;
+    spgemm<B, B, K>(c, view(L), Pt, L.Prp, L.Pci, L.Tval, tn);
+    tick(c, "A*Pt", lvl);
+    L.Pnnzb = tn;
+    L.Pval.ensure(c.al, (size_t)tn * B * K);
+    k_smooth_p<B, K><<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.Prp.get(), L.Pci.get(), L.Tval.get(), L.dinv.get(),
+                                                      L.agg.get(), ptrp, ptval, omega, L.Pval.get());
+    SI_LAUNCHED(c);
+  }
   L.nbc = na;
   BsrMat P{nb, na, B, K, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.Pval.get()};
   tick(c, "smoothP", lvl);
@@ -2394,8 +2518,9 @@ void amg_setup_impl(Ctx& c) {
   L0.val.ensure(c.al, (size_t)L0.nnzb * 4);
   k_stencil_to_bsr<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L0.rp.get(), L0.val.get());
   SI_LAUNCHED(c);
-  const int K = c.p.nullspace_dim;
+  int K = c.p.nullspace_dim;
   SI_CHECK(K == 3 || c.lin_v.get(), SEAICE_ESTATE, "nullspace_dim = 4 needs an assembled linearisation point");
+  if (K == 4 && norm2(c, c.lin_v.get(), c.N) == 0.0) K = 3;  // reading G30: v_l = 0 adds no column
   L0.B.ensure(c.al, (size_t)c.Nn * 2 * K);
   k_level0_nullspace<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.p.L, K, c.lin_v.get(), L0.B.get());
   SI_LAUNCHED(c);

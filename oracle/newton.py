@@ -27,7 +27,8 @@ def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
     """forcing = 1: Eisenstat-Walker choice 2 for the Krylov tolerance of each solve (reading
     G29, DESIGN.md): eta_0 = 0.1, eta_l = 0.9 (|R_l|/|R_{l-1}|)^2, safeguards
     eta_l >= 0.9 eta_{l-1}^2 (if > 0.1) and eta_l >= 0.5 rtol |R_0|/|R_l|, clamped to
-    [krylov_rtol, 0.1].
+    [krylov_rtol, 0.1]; after a line search that found no decrease (stagnation flag) the next
+    solve uses krylov_rtol.
     amg_lag = T > 0 (reading G31): at Newton iteration l >= 1 the AMG hierarchy is rebuilt only
     if the previous linear solve needed more than T Krylov iterations; otherwise its coarse
     levels are kept and only the finest level is refreshed from the current Jacobian
@@ -66,6 +67,10 @@ def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
                     eta = max(eta, 0.9 * eta_prev ** 2)
             eta = max(eta, 0.5 * rtol * r0 / nr)
             eta = min(max(eta, krylov_rtol), 0.1)
+            if l > 0 and hist["stagnated"][-1]:
+                # safeguard: the last line search found no energy decrease (the inexact
+                # direction was not a descent direction): solve to the floor tolerance
+                eta = krylov_rtol
             eta_prev = eta
             krtol = eta
         pi_j = pi if kind == "sv" else None

@@ -129,6 +129,9 @@ int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* o
       }
       eta = std::max(eta, 0.5 * c.p.newton_rtol * c.r0 / st.res_norm);
       eta = std::min(std::max(eta, rtol_fixed), 0.1);
+      // safeguard: after a line search that found no energy decrease the inexact direction was
+      // not a descent direction; solve the next system to the floor tolerance
+      if (c.ew_ls_failed) eta = rtol_fixed;
       c.ew_prev_res = st.res_norm;
       c.ew_prev_eta = eta;
       c.p.krylov_rtol = eta;
@@ -173,6 +176,7 @@ int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* o
         }
       }
     }
+    c.ew_ls_failed = acc < 0;  // EW safeguard for the next solve (reading G29)
     if (acc < 0) {
       st.ls_stagnated = 1;
       acc = K - 1;

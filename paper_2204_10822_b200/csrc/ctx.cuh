@@ -158,6 +158,7 @@ struct Ctx {
   bool have_r0 = false;
   double r0 = 0.0;
   double ew_prev_res = 0.0, ew_prev_eta = 0.0;  // Eisenstat-Walker state of the current step
+  bool ew_ls_failed = false;                     // last line search found no decrease
   DBuf<double> vt, pit;
 
   // Krylov

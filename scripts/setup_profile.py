@@ -60,7 +60,7 @@ for ln in lines:
     if not m:
         continue
     lvl, what, ms = m.group(1), m.group(2).strip(), float(m.group(3))
-    key = f"{what} rows={lvl}" if what.startswith("sg.") else f"L{lvl} {what}"
+    key = what if what.startswith("sg.") else f"L{lvl} {what}"  # SpGEMM ticks carry row counts, not levels
     tot[key] += ms
     if what == "graph_free":
         nset += 1

@@ -279,11 +279,14 @@ int64_t seaice_launch_count(const seaice_ctx* ctx);
  * each launch.  Classes: 0 assembly (K1), 1 finest SpMV, 2 finest Chebyshev step,
  * 3 coarse Chebyshev step, 4 finest residual+Dinv, 5 Krylov multi-dot, 6 multi-axpy+norm,
  * 7 solution update, 8 line-search energy, 9 restriction/prolongation, 10 coarse solve,
- * 11 coarse residual+Dinv, 12 dual update.  enable: resets the counters and turns the
+ * 11 coarse residual+Dinv (levels >= 2), 12 dual update, 13 fused finest Chebyshev(3),
+ * 14 transport, 15 matrix-free apply, 16 Chebyshev step on level 1, 17 residual+Dinv on level 1,
+ * 18 restriction/prolongation between levels 0 and 1 (9: deeper levels; 3: coarse Chebyshev on
+ * levels >= 2).  enable: resets the counters and turns the
  * timing on (1) or off (0).  read: synchronizes, returns total milliseconds, launch
  * counts and algorithmic bytes (DESIGN.md formulas) per class (arrays of
  * SEAICE_PROF_CLASSES; any pointer may be NULL). */
-#define SEAICE_PROF_CLASSES 16
+#define SEAICE_PROF_CLASSES 24
 int seaice_profile_enable(seaice_ctx* ctx, int32_t on);
 int seaice_profile_read(seaice_ctx* ctx, double* ms_host, int64_t* launches_host, double* alg_bytes_host);
 

@@ -2671,7 +2671,7 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
     const double B = L.b;
     double by = L.nb * (8.0 * B * 3 + 8.0 * B * B);  // b read, r write, d write, dinv
     if (!pre) by += (st ? kJBytesNode * c.Nn : L.nnzb * (8.0 * B * B + 4.0) + 4.0 * (L.nb + 1)) + 8.0 * B * L.nb;
-    prof_end(c, st ? PC_RESID0 : PC_RESIDC, by);
+    prof_end(c, st ? PC_RESID0 : (l == 1 ? PC_RESID1 : PC_RESIDC), by);
   }
   if (fused) {
     ChebFCoef kc;
@@ -2731,7 +2731,7 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
       double by = L.nb * 8.0 * B * (first ? 2.0 : 3.0);  // d read, x (read +) write
       if (want_r) by += (st ? kJBytesNode * c.Nn : L.nnzb * (8.0 * B * B + 4.0) + 4.0 * (L.nb + 1)) + 16.0 * B * L.nb;
       if (want_d) by += L.nb * (8.0 * B * B + 8.0 * B);
-      prof_end(c, st ? PC_CHEB0 : PC_CHEBC, by);
+      prof_end(c, st ? PC_CHEB0 : (l == 1 ? PC_CHEB1 : PC_CHEBC), by);
     }
     rho = rho_new;
     std::swap(d, d2);
@@ -2753,14 +2753,14 @@ static void vcycle_level(Ctx& c, int l, const double* b, double* x) {
   prof_begin(c);
   gspmv(c, L.nbc, Lc.b, L.b, L.Rnnzb, L.Rrp.get(), L.Rci.get(), Lc.b == 4 ? L.Rval.get() : L.RvalT.get(), L.r.get(),
         nullptr, Lc.rhs.get());
-  prof_end(c, PC_TRANSFER,
+  prof_end(c, l == 0 ? PC_TRANSFER0 : PC_TRANSFER,
            L.Rnnzb * (8.0 * Lc.b * L.b + 4.0) + 4.0 * (L.nbc + 1) + 8.0 * L.b * L.nb + 8.0 * Lc.b * L.nbc);
   vcycle_level(c, l + 1, Lc.rhs.get(), Lc.x.get());
   // x += P e_c
   prof_begin(c);
   gspmv(c, L.nb, L.b, Lc.b, L.Pnnzb, L.Prp.get(), L.Pci.get(), Lc.b == 4 ? L.Pval.get() : L.PvalT.get(), Lc.x.get(),
         x, x);
-  prof_end(c, PC_TRANSFER,
+  prof_end(c, l == 0 ? PC_TRANSFER0 : PC_TRANSFER,
            L.Pnnzb * (8.0 * Lc.b * L.b + 4.0) + 4.0 * (L.nb + 1) + 16.0 * L.b * L.nb + 8.0 * Lc.b * L.nbc);
   smooth(c, l, b, x, false);
 }

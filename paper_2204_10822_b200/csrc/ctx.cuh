@@ -99,7 +99,10 @@ enum ProfClass {
   PC_CHEB0F = 13,   // K4 three Chebyshev steps fused (temporal blocking), finest level
   PC_TRANSPORT = 14,  // NEXT-3 explicit upwind transport of A, h
   PC_MATFREE = 15,  // NEXT-4 matrix-free Jacobian apply
-  PC_NCLASS = 16
+  PC_CHEB1 = 16,    // K4 Chebyshev step on level 1 (PC_CHEBC: levels >= 2)
+  PC_RESID1 = 17,   // residual + Dinv on level 1 (PC_RESIDC: levels >= 2)
+  PC_TRANSFER0 = 18,  // restriction / prolongation between levels 0 and 1 (PC_TRANSFER: deeper)
+  PC_NCLASS = 19
 };
 struct Prof {
   bool on = false;

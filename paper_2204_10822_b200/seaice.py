@@ -266,15 +266,16 @@ class SeaIce:
         return int(self.L.seaice_launch_count(self.h))
 
     PROF_NAMES = ["assemble", "spmv0", "cheb0", "cheb_coarse", "resid0", "multidot", "maxpy_norm", "maxpy",
-                  "delta_energy", "transfer", "coarse_solve", "resid_coarse", "pi_update", "cheb0_fused", "transport", "jv_matfree"]
+                  "delta_energy", "transfer", "coarse_solve", "resid_coarse", "pi_update", "cheb0_fused", "transport",
+                  "jv_matfree", "cheb_level1", "resid_level1", "transfer_level0"]
 
     def profile(self, on: bool):
         self._check(self.L.seaice_profile_enable(self.h, 1 if on else 0))
 
     def profile_read(self):
-        ms = (C.c_double * 16)()
-        cnt = (C.c_int64 * 16)()
-        by = (C.c_double * 16)()
+        ms = (C.c_double * 24)()
+        cnt = (C.c_int64 * 24)()
+        by = (C.c_double * 24)()
         self._check(self.L.seaice_profile_read(self.h, ms, cnt, by))
         return {name: {"ms": ms[k], "launches": cnt[k], "bytes": by[k]} for k, name in enumerate(self.PROF_NAMES)}
 

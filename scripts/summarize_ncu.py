@@ -78,6 +78,22 @@ if os.path.exists(os.path.join(G, "vc_launches.csv")):
                 per[c][0] += 1
                 per[c][1] += rb + wb
                 per[c][2] += us
+    # level-specific classes (bench.py's cheb_level1 / resid_level1 / transfer_level0): the level-1
+    # launches are the k_acheb4 / k_aresid4 launches with the largest grid, the level-0 transfers
+    # the k_aspmv launches with 2-row or 2-column blocks
+    def gx(d):
+        return int(d["grid"].strip("()").split(",")[0])
+    for kname, cls in (("k_acheb4", "cheb_level1"), ("k_aresid4", "resid_level1")):
+        ds = [d for d in V.values() if kname in d["name"]]
+        if ds:
+            g = max(gx(d) for d in ds)
+            sel = [d for d in ds if gx(d) == g]
+            per[cls] = [len(sel), sum(d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+                                      for d in sel), 0.0]
+    sel = [d for d in V.values() if "k_aspmv<4, 2" in d["name"] or "k_aspmv<2, 4" in d["name"]]
+    if sel:
+        per["transfer_level0"] = [len(sel), sum(d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+                                                for d in sel), 0.0]
     for c, (n, b, us) in per.items():
         traffic[c] = b / n
     print("V-cycle launches:", len(V))

@@ -80,8 +80,9 @@ typedef struct {
   int32_t power_iters;     /* power iterations for lambda_max(D^-1 A) */
   int32_t project_pi;      /* 0 (default): store pi unprojected (reading G5) */
   uint64_t amg_seed;
-  int32_t agg_dist0;       /* aggregation root distance on the finest level: 2 = MIS(2) (default), 1 = MIS(1) */
-  int32_t agg_dist;        /* same on coarse levels */
+  int32_t agg_dist0;       /* aggregation root distance on the finest level: 2 = MIS(2) (default), 1 = MIS(1),
+                              3 = MIS(3) (larger aggregates) */
+  int32_t agg_dist;        /* same on coarse levels (default 3) */
   int32_t cheb_fused;      /* 1 (default): finest-level Chebyshev(3) as one temporally blocked launch
                               (same arithmetic per node and step); 0: one launch per step */
   int32_t cheb_degree0;    /* Chebyshev degree on the finest level (0: cheb_degree) */

@@ -99,7 +99,7 @@ def strength(A, b, theta):
 
 def mis2(G, seed, level, dist=2):
     """Round-synchronous MIS(2) on the strength graph G (definition in the module header);
-    dist=1 gives MIS(1) (one max pass per round)."""
+    dist = d gives MIS(d) (d closed-neighbourhood max passes per round, d = 1..3)."""
     nb = G.shape[0]
     deg = np.diff(G.indptr)
     isolated = deg == 0
@@ -111,8 +111,9 @@ def mis2(G, seed, level, dist=2):
     rounds = 0
     while np.any(state == 1):
         key = (state << np.uint64(62)) | (h << np.uint64(25)) | idx
-        T1 = np.maximum.reduceat(key[C.indices], C.indptr[:-1])
-        T2 = np.maximum.reduceat(T1[C.indices], C.indptr[:-1]) if dist == 2 else T1
+        T2 = key
+        for _ in range(dist):
+            T2 = np.maximum.reduceat(T2[C.indices], C.indptr[:-1])
         und = state == 1
         new_in = und & (T2 == key)
         new_out = und & ~new_in & ((T2 >> np.uint64(62)) == 2)
@@ -245,7 +246,7 @@ def level0_nullspace(n, L, v=None):
 
 
 def setup(J, pb=None, theta=0.04, coarse_max_dof=400, max_levels=25, power_iters=20, seed=0,
-          cheb_degree=3, cheb_lower=0.03, cheb_upper=1.1, n=None, L=512e3, agg_dist0=2, agg_dist=2,
+          cheb_degree=3, cheb_lower=0.03, cheb_upper=1.1, n=None, L=512e3, agg_dist0=2, agg_dist=3,
           v=None, nullspace_dim=4):
     """nullspace_dim = 4 (reading G30) appends the linearisation point v (required then) to
     the three rigid-body modes; coarse levels then carry 4 x 4 blocks.  If v is identically

@@ -2308,13 +2308,17 @@ static int aggregate_level(Ctx& c, Level& L, int lvl, const double* dnorm, Scrat
   int* und = S.get<int>(1);
   k_mis_init<<<grid_for(nb), kThreads, 0, c.s>>>(nb, grp, salt(c.p.amg_seed, lvl, 1), key);
   SI_LAUNCHED(c);
-  const int dist = (lvl == 0) ? c.p.agg_dist0 : c.p.agg_dist;  // MIS(2) or MIS(1)
+  const int dist = (lvl == 0) ? c.p.agg_dist0 : c.p.agg_dist;  // MIS(d), d = 1..3
   for (int round = 0;; ++round) {
     SI_CHECK(round < 10000, SEAICE_ECUDA, "MIS did not terminate");
-    k_mis_max<<<grid_for(nb), kThreads, 0, c.s>>>(nb, grp, gci, key, T1);
-    if (dist == 2) k_mis_max<<<grid_for(nb), kThreads, 0, c.s>>>(nb, grp, gci, T1, T2);
+    const unsigned long long* tin = key;
+    for (int p = 0; p < dist; ++p) {  // closed-neighbourhood max, dist times (ping-pong T1 / T2)
+      unsigned long long* tout = (p & 1) ? T2 : T1;
+      k_mis_max<<<grid_for(nb), kThreads, 0, c.s>>>(nb, grp, gci, tin, tout);
+      tin = tout;
+    }
     SI_CUDA(cudaMemsetAsync(und, 0, sizeof(int), c.s));
-    k_mis_update<<<grid_for(nb), kThreads, 0, c.s>>>(nb, key, dist == 2 ? T2 : T1, und);
+    k_mis_update<<<grid_for(nb), kThreads, 0, c.s>>>(nb, key, tin, und);
     SI_LAUNCHED(c);
     c.launches += dist;
     if (read_scalar(c, und) == 0) break;

@@ -219,3 +219,21 @@ def test_refresh_finest_keeps_coarse_levels_and_symmetry():
     r1, r2 = rng.standard_normal(J.shape[0]), rng.standard_normal(J.shape[0])
     z1, z2 = amg.vcycle(H2, r1), amg.vcycle(H2, r2)
     assert abs(z1 @ r2 - r1 @ z2) <= 1e-10 * abs(z1 @ r2)
+
+
+@pytest.mark.parametrize("dist", [1, 3])
+def test_misd_is_distance_d_independent_and_maximal(dist):
+    """MIS(d) for the agg_dist options: no two roots within graph distance d, every non-isolated
+    node within distance d of a root (brute-force reachability by powers of the closed graph)."""
+    pb, J = _jacobian(20)
+    G = amg.strength(J, 2, 0.04)
+    roots, isolated, _ = amg.mis2(G, 0, 0, dist=dist)
+    C = (G + sp.identity(G.shape[0], format="csr")).tocsr()
+    Cd = C.copy()
+    for _ in range(dist - 1):
+        Cd = (Cd @ C).tocsr()
+    R = np.where(roots)[0]
+    sub = Cd[R][:, R].tocoo()
+    assert np.all(sub.row == sub.col), f"two roots within distance {dist}"
+    covered = np.asarray(Cd[:, R].sum(axis=1)).ravel() > 0
+    assert np.all(covered | isolated)

@@ -106,12 +106,19 @@ typedef struct {
                               to force one path for every product: 1 hash tables (1k, else 4k
                               entries, else sort), 2 sort + thread-per-row numeric, 3 sort + 8-lane
                               groups, 4 sort + warp per row, 5 8-lane hash tables (falls back when a
-                              row's expansion exceeds 256) (see seaice_spgemm_path_hits) */
+                              row's expansion exceeds 256), 6 hash tables of 4k entries (else sort)
+                              (see seaice_spgemm_path_hits) */
   int32_t amg_lag;         /* 0: full AMG setup at every Newton iteration; T > 0 (reading G31):
                               at Newton iteration l >= 1 of a time step the hierarchy is rebuilt only
                               if the previous linear solve needed more than T Krylov iterations,
                               otherwise its coarse levels (P, R, A_l, l >= 1) are kept and only the
                               finest level (D^-1 blocks, lambda_max) is refreshed from the current J */
+  int32_t amg_reuse;       /* 0: every AMG setup builds its aggregates; 1 (reading G32): the
+                              first setup of a time step builds them, every later setup of the step
+                              keeps the aggregates and all sparsity patterns (P_tent, P, R, Galerkin
+                              products) and recomputes every value from the current J and v_l
+                              (near-nullspace, P_tent, lambda_max, smoothed P, A_l, coarse factor);
+                              falls back to a full setup when the near-nullspace dimension changes */
 } seaice_params;
 
 /* Compressed-sparse-row view (scalar rows). Index arrays int32, values fp64. */
@@ -148,6 +155,7 @@ typedef struct {
   double amg_op_complexity;
   double t_assemble, t_amg, t_krylov, t_ls; /* milliseconds (CUDA events) */
   int32_t amg_rebuilt;      /* 1: full AMG setup this iteration; 0: coarse levels kept (amg_lag) */
+  int32_t amg_reused;       /* 1: the setup kept the step's aggregates and patterns (amg_reuse) */
 } seaice_newton_stats;
 
 typedef struct {
@@ -160,6 +168,7 @@ typedef struct {
                                step still used the capped iterate) */
   int32_t krylov_max_iters; /* largest iteration count of one solve */
   int32_t amg_setups;       /* full AMG setups in the step (< newton_iters with amg_lag) */
+  int32_t amg_reuses;       /* of those, setups that kept the aggregates and patterns (amg_reuse) */
 } seaice_step_stats;
 
 /* Default parameters (Table 1 + BASELINE.json + DESIGN.md readings) for mesh size n. */

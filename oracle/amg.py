@@ -31,6 +31,11 @@ Definition (every choice is a parameter; both sides implement it independently):
   coarse op  A_c = P^T (A P); coarse DOFs whose diagonal is exactly 0 (dropped columns) get 1.
   recursion  stop when 3 n_agg <= coarse_max_dof, at max_levels, or when n_agg > 0.9 n_nodes.
   coarsest   dense Cholesky solve.
+  reuse      (reading G32, `reuse=H_prev`) the aggregates of H_prev are kept level by level (no
+             strength graph / MIS / aggregation; same level count), everything else — near-
+             nullspace with the current v, P_tent, lambda, smoothed P, Galerkin operators,
+             coarse factor — is recomputed from the current J.  Ignored (full setup) when the
+             near-nullspace dimension differs from H_prev's.
   smoother   Chebyshev of degree m for D^-1 A on [lo b, b], b = up * lambda (Saad Alg. 12.1):
              th = (b+a)/2, de = (b-a)/2, sg = th/de, rho = 1/sg, d = D^-1 r/th;
              repeat m times: x += d; r -= A d; rho' = 1/(2 sg - rho); d = rho' rho d + 2 rho'/de D^-1 r.
@@ -247,7 +252,7 @@ def level0_nullspace(n, L, v=None):
 
 def setup(J, pb=None, theta=0.04, coarse_max_dof=400, max_levels=25, power_iters=20, seed=0,
           cheb_degree=3, cheb_lower=0.03, cheb_upper=1.1, n=None, L=512e3, agg_dist0=2, agg_dist=3,
-          v=None, nullspace_dim=4):
+          v=None, nullspace_dim=4, reuse=None):
     """nullspace_dim = 4 (reading G30) appends the linearisation point v (required then) to
     the three rigid-body modes; coarse levels then carry 4 x 4 blocks.  If v is identically
     zero the three rigid-body modes are used (3 x 3 coarse blocks)."""
@@ -261,20 +266,29 @@ def setup(J, pb=None, theta=0.04, coarse_max_dof=400, max_levels=25, power_iters
         nullspace_dim = 3  # reading G30: v_l = 0 (e.g. the first iterate from rest) adds no column
     B = level0_nullspace(n, L, v if nullspace_dim == 4 else None)
     K = B.shape[1]
+    if reuse is not None and reuse.get("K") != K:
+        reuse = None  # reading G32: a different near-nullspace dimension changes the block size
+    keep = reuse["levels"] if reuse is not None else None
     levels = []
     for lvl in range(max_levels):
         Dinv, blocks = block_diag_inv(A, b)
         lev = {"A": A, "b": b, "Dinv": Dinv, "nb": A.shape[0] // b}
         lev["lmax"] = lambda_max(A, Dinv, seed, lvl, power_iters)
         levels.append(lev)
-        if A.shape[0] <= coarse_max_dof or lvl + 1 == max_levels:
-            break
-        G = strength(A, b, theta)
-        roots, isolated, rounds = mis2(G, seed, lvl, agg_dist0 if lvl == 0 else agg_dist)
-        agg = aggregate(G, roots, isolated)
-        na = int(roots.sum())
-        if na == 0 or na > 0.9 * lev["nb"]:
-            break
+        if keep is not None:
+            if lvl == len(keep) - 1:
+                break
+            agg, roots, rounds = keep[lvl]["agg"], keep[lvl]["roots"], 0
+            na = int(roots.sum())
+        else:
+            if A.shape[0] <= coarse_max_dof or lvl + 1 == max_levels:
+                break
+            G = strength(A, b, theta)
+            roots, isolated, rounds = mis2(G, seed, lvl, agg_dist0 if lvl == 0 else agg_dist)
+            agg = aggregate(G, roots, isolated)
+            na = int(roots.sum())
+            if na == 0 or na > 0.9 * lev["nb"]:
+                break
         Pt, Bc, na = tentative(agg, B, b)
         omega = 4.0 / (3.0 * lev["lmax"])
         P = (Pt - omega * (Dinv @ (A @ Pt))).tocsr()
@@ -290,6 +304,7 @@ def setup(J, pb=None, theta=0.04, coarse_max_dof=400, max_levels=25, power_iters
     coarse["chol"] = sla.cho_factor(coarse["A"].toarray(), lower=True)
     nnz0 = levels[0]["A"].nnz
     return {"levels": levels, "cheb_degree": cheb_degree, "cheb_lower": cheb_lower, "cheb_upper": cheb_upper,
+            "K": K, "reused": keep is not None,
             "op_complexity": sum(l["A"].nnz for l in levels) / nnz0}
 
 

@@ -23,7 +23,8 @@ LS_ETA = 1e-12
 
 def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
                ls_max=20, krylov_rtol=1e-8, krylov_maxit=300, restart=30,
-               project_pi=False, amg_params=None, record_iterates=False, forcing=0, amg_lag=0):
+               project_pi=False, amg_params=None, record_iterates=False, forcing=0, amg_lag=0,
+               amg_reuse=0):
     """forcing = 1: Eisenstat-Walker choice 2 for the Krylov tolerance of each solve (reading
     G29, DESIGN.md): eta_0 = 0.1, eta_l = 0.9 (|R_l|/|R_{l-1}|)^2, safeguards
     eta_l >= 0.9 eta_{l-1}^2 (if > 0.1) and eta_l >= 0.5 rtol |R_0|/|R_l|, clamped to
@@ -32,7 +33,10 @@ def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
     amg_lag = T > 0 (reading G31): at Newton iteration l >= 1 the AMG hierarchy is rebuilt only
     if the previous linear solve needed more than T Krylov iterations; otherwise its coarse
     levels are kept and only the finest level is refreshed from the current Jacobian
-    (amg.refresh_finest)."""
+    (amg.refresh_finest).
+    amg_reuse = 1 (reading G32): the first AMG setup of the time step builds the aggregates;
+    every later setup of the step keeps them (amg.setup(..., reuse=H)) and recomputes all values
+    from the current Jacobian and linearisation point."""
     pb = Problem(inp, prm)
     v = pb.v_prev.copy()
     v[pb.bdof] = 0.0
@@ -89,8 +93,9 @@ def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
             # amg_params["nullspace_dim"] == 4 (reading G30); ignored otherwise
             ap = amg_params or {}
             if H is None or amg_lag <= 0 or hist["krylov"][-1]["iters"] > amg_lag:
-                H = amg.setup(J, pb, v=v, **ap)
+                H = amg.setup(J, pb, v=v, reuse=H if amg_reuse else None, **ap)
                 hist.setdefault("amg_rebuilt", []).append(True)
+                hist.setdefault("amg_reused", []).append(H["reused"])
             else:
                 H = amg.refresh_finest(H, J, seed=ap.get("seed", 0), power_iters=ap.get("power_iters", 20))
                 hist.setdefault("amg_rebuilt", []).append(False)

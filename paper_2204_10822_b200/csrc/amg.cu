@@ -1047,11 +1047,60 @@ struct BsrMat {
   double* val = nullptr;
 };
 
-// Small levels: CTA-per-row numeric if every row's pattern fits the shared accumulators.
-// Returns true if it ran (crp / cci / cval already sized, pattern written).
+// Numeric phase of C = X Y on C's (already built) pattern, by the kernel the plan names.  Every
+// kernel accumulates each output block over X entries in row order, so all kinds give bitwise
+// the same values; the full setup records the kind it chose, the numeric-only setup of reading
+// G32 replays it on the kept pattern.
 template <int M, int K, int P>
-static bool cta_numeric(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBuf<int>& cci,
-                        DBuf<double>& cval, const int* cnt, Scratch& S) {
+static void sg_numeric(Ctx& c, const SgPlan& pl, const BsrMat& X, const BsrMat& Y, const int* crp, const int* cci,
+                       double* cval) {
+  const int nr = X.nbr;
+  if (nr == 0) return;
+  switch (pl.kind) {
+    case SG_NARROW:
+      k_sgn_numeric<M, K, P><<<(nr + 1 + kNRows - 1) / kNRows, 32 * kNW, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci,
+                                                                                  Y.val, crp, cci, cval);
+      break;
+    case SG_HASH1K:
+      k_sg_hash_numeric<M, K, P, kHT, kHWarps><<<(nr + 1 + kHWarps - 1) / kHWarps, 32 * kHWarps, 0, c.s>>>(
+          nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp, cci, cval);
+      break;
+    case SG_HASH4K:
+      k_sg_hash_numeric<M, K, P, kHT2, kHWarps2><<<(nr + 1 + kHWarps2 - 1) / kHWarps2, 32 * kHWarps2, 0, c.s>>>(
+          nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp, cci, cval);
+      break;
+    case SG_CTA: {
+      static bool attr_set = false;
+      if (!attr_set) {
+        SI_CUDA(cudaFuncSetAttribute(k_sg_cta_numeric<M, K, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kCtaMaxCols * (M * P * (int)sizeof(double) + (int)sizeof(int)) + 16));
+        attr_set = true;
+      }
+      k_sg_cta_numeric<M, K, P><<<nr, 256, pl.smem, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp, cci, cval);
+      break;
+    }
+    case SG_THREAD:
+      k_spgemm_numeric<M, K, P><<<grid_for(nr, 128), 128, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp,
+                                                                     cci, cval);
+      break;
+    case SG_GROUP8:
+      k_spgemm_numeric_g<M, K, P, 8><<<(int)(((long long)nr * 8 + 255) / 256), 256, 0, c.s>>>(
+          nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp, cci, cval);
+      break;
+    case SG_WARP:
+      k_spgemm_numeric_w<M, K, P><<<wgrid(nr), 256, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp, cci,
+                                                               cval);
+      break;
+    default:
+      SI_CHECK(false, SEAICE_ESTATE, "SpGEMM numeric phase without a plan");
+  }
+  SI_LAUNCHED(c);
+}
+
+// Small levels: CTA-per-row numeric if every row's pattern fits the shared accumulators.
+// Returns true (and records SG_CTA in the plan) if it applies.
+template <int M, int K, int P>
+static bool cta_numeric(Ctx& c, const BsrMat& X, const int* cnt, SgPlan& pl, Scratch& S) {
   const int nr = X.nbr;
   if (nr > kCtaRows || c.p.spgemm_path != 0) return false;
   int* mx = S.get<int>(1);
@@ -1062,16 +1111,8 @@ static bool cta_numeric(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp
   c.launches += 1;
   const int umax = read_scalar(c, mx);
   if (umax > kCtaMaxCols) return false;
-  const size_t smem = (size_t)umax * (M * P * sizeof(double) + sizeof(int)) + 16;
-  static bool attr_set = false;
-  if (!attr_set) {
-    SI_CUDA(cudaFuncSetAttribute(k_sg_cta_numeric<M, K, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kCtaMaxCols * (M * P * (int)sizeof(double) + (int)sizeof(int)) + 16));
-    attr_set = true;
-  }
-  k_sg_cta_numeric<M, K, P><<<nr, 256, smem, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp.get(), cci.get(),
-                                                     cval.get());
-  SI_LAUNCHED(c);
+  pl.kind = SG_CTA;
+  pl.smem = (size_t)umax * (M * P * sizeof(double) + sizeof(int)) + 16;
   c.sg_hits[6]++;
   return true;
 }
@@ -1079,7 +1120,7 @@ static bool cta_numeric(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp
 // hash path: every row's expansion fits the per-warp shared-memory table of HT slots
 template <int M, int K, int P, int HT, int HW>
 static void hash_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBuf<int>& cci,
-                        DBuf<double>& cval, long long& cnnzb, Scratch& S) {
+                        DBuf<double>& cval, long long& cnnzb, SgPlan& pl, Scratch& S) {
   const int nr = X.nbr;
   const int hb = (nr + 1 + HW - 1) / HW;
   int* cnt = S.get<int>(nr + 1);
@@ -1093,17 +1134,14 @@ static void hash_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp
   cval.ensure(c.al, cnnzb * M * P);
   k_sg_hash_cols<HT, HW><<<hb, 32 * HW, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, crp.get(), cci.get());
   SI_LAUNCHED(c);
-  if (!cta_numeric<M, K, P>(c, X, Y, crp, cci, cval, cnt, S)) {
-    k_sg_hash_numeric<M, K, P, HT, HW><<<hb, 32 * HW, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val,
-                                                                 crp.get(), cci.get(), cval.get());
-    SI_LAUNCHED(c);
-  }
+  if (!cta_numeric<M, K, P>(c, X, cnt, pl, S)) pl.kind = (HT == kHT) ? SG_HASH1K : SG_HASH4K;
+  sg_numeric<M, K, P>(c, pl, X, Y, crp.get(), cci.get(), cval.get());
   tick(c, HT == kHT ? "  sg.hash1k" : "  sg.hash4k", nr);
 }
 
 template <int M, int K, int P>
 static void narrow_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBuf<int>& cci,
-                          DBuf<double>& cval, long long& cnnzb, Scratch& S) {
+                          DBuf<double>& cval, long long& cnnzb, SgPlan& pl, Scratch& S) {
   const int nr = X.nbr;
   const int hb = (nr + 1 + kNRows - 1) / kNRows;
   int* cnt = S.get<int>(nr + 1);
@@ -1117,16 +1155,16 @@ static void narrow_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& c
   cval.ensure(c.al, cnnzb * M * P);
   k_sgn_cols<<<hb, 32 * kNW, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, crp.get(), cci.get());
   SI_LAUNCHED(c);
-  k_sgn_numeric<M, K, P><<<hb, 32 * kNW, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp.get(), cci.get(),
-                                                    cval.get());
-  SI_LAUNCHED(c);
+  pl.kind = SG_NARROW;
+  sg_numeric<M, K, P>(c, pl, X, Y, crp.get(), cci.get(), cval.get());
   tick(c, "  sg.narrow", nr);
 }
 
 // Output arrays are grow-only DBufs owned by the caller.
 template <int M, int K, int P>
 static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBuf<int>& cci, DBuf<double>& cval,
-                   long long& cnnzb) {
+                   long long& cnnzb, SgPlan& pl) {
+  pl = SgPlan{};
   const int nr = X.nbr;
   Scratch S(c);
   long long* ub = S.get<long long>(nr + 1);
@@ -1149,18 +1187,18 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
     const double ylen = Y.nbr > 0 ? (double)Y.nnzb / Y.nbr : 1.0;
     if ((force == 5 || (force == 0 && ylen <= 12.0 && tot >= 24LL * nr)) && maxub <= kNHT / 2) {
       c.sg_hits[5]++;
-      narrow_spgemm<M, K, P>(c, X, Y, crp, cci, cval, cnnzb, S);
+      narrow_spgemm<M, K, P>(c, X, Y, crp, cci, cval, cnnzb, pl, S);
       return;
     }
-    const bool wide_rows = force == 1 || (force == 0 && tot >= 32LL * nr);
-    if (wide_rows && maxub <= kHT / 2) {
+    const bool wide_rows = force == 1 || force == 6 || (force == 0 && tot >= 32LL * nr);
+    if (wide_rows && maxub <= kHT / 2 && force != 6) {
       c.sg_hits[0]++;
-      hash_spgemm<M, K, P, kHT, kHWarps>(c, X, Y, crp, cci, cval, cnnzb, S);
+      hash_spgemm<M, K, P, kHT, kHWarps>(c, X, Y, crp, cci, cval, cnnzb, pl, S);
       return;
     }
     if (wide_rows && maxub <= kHT2 / 2) {
       c.sg_hits[1]++;
-      hash_spgemm<M, K, P, kHT2, kHWarps2>(c, X, Y, crp, cci, cval, cnnzb, S);
+      hash_spgemm<M, K, P, kHT2, kHWarps2>(c, X, Y, crp, cci, cval, cnnzb, pl, S);
       return;
     }
   }
@@ -1171,7 +1209,7 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
   int* k1 = S.get<int>(total);
   int* k2 = S.get<int>(total);
   const int force = c.p.spgemm_path;
-  const bool wide = force == 4 || ((force == 0 || force == 1) && total > 48LL * nr);  // long rows: warp per row
+  const bool wide = force == 4 || ((force == 0 || force == 1 || force == 6) && total > 48LL * nr);  // long rows: warp per row
   if (wide)
     k_spgemm_expand_w<<<wgrid(nr), 256, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, off, k1);
   else
@@ -1200,25 +1238,19 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
   SI_CHECK(cnnzb < (1LL << 31), SEAICE_EINVAL, "SpGEMM result exceeds int32 indexing");
   cci.ensure(c.al, cnnzb);
   cval.ensure(c.al, cnnzb * M * P);
-  const bool thread_numeric = force == 2 || ((force == 0 || force == 1) && Y.nbr > 0 && (double)Y.nnzb / Y.nbr <= 6.0);
+  const bool thread_numeric = force == 2 || ((force == 0 || force == 1 || force == 6) && Y.nbr > 0 && (double)Y.nnzb / Y.nbr <= 6.0);
   c.sg_hits[wide ? 4 : thread_numeric ? 2 : 3]++;
   if (wide) {
     k_spgemm_compact_w<<<wgrid(nr), 256, 0, c.s>>>(nr, off, k1, crp.get(), cci.get());
     SI_LAUNCHED(c);
-    if (!cta_numeric<M, K, P>(c, X, Y, crp, cci, cval, cnt, S))
-      k_spgemm_numeric_w<M, K, P><<<wgrid(nr), 256, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp.get(),
-                                                              cci.get(), cval.get());
+    if (!cta_numeric<M, K, P>(c, X, cnt, pl, S)) pl.kind = SG_WARP;
   } else {
     k_spgemm_compact<<<grid_for(nr), kThreads, 0, c.s>>>(nr, off, k1, crp.get(), cci.get());
     SI_LAUNCHED(c);
-    if (thread_numeric)  // measured: thread per row beats 4-lane groups for the finest level
-      k_spgemm_numeric<M, K, P><<<grid_for(nr, 128), 128, 0, c.s>>>(nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val,
-                                                                     crp.get(), cci.get(), cval.get());
-    else
-      k_spgemm_numeric_g<M, K, P, 8><<<(int)(((long long)nr * 8 + 255) / 256), 256, 0, c.s>>>(
-          nr, X.rp, X.ci, X.val, Y.rp, Y.ci, Y.val, crp.get(), cci.get(), cval.get());
+    // measured: thread per row beats 4-lane groups for the finest level
+    pl.kind = thread_numeric ? SG_THREAD : SG_GROUP8;
   }
-  SI_LAUNCHED(c);
+  sg_numeric<M, K, P>(c, pl, X, Y, crp.get(), cci.get(), cval.get());
   tick(c, wide ? "  sg.numericW" : "  sg.numeric", (int)(total / std::max(nr, 1)));
 }
 
@@ -1246,13 +1278,18 @@ __global__ void k_transpose_gather(long long nnz, const int* __restrict__ perm, 
 }
 
 // T (BC x BR blocks) = X^T for X (BR x BC blocks)
+// perm / rowof keep the gather map (entry k of T is entry perm[k] of X, in row rowof[perm[k]])
+// for the numeric-only setup (reading G32).
 template <int BR, int BC>
-static void transpose(Ctx& c, const BsrMat& X, DBuf<int>& trp, DBuf<int>& tci, DBuf<double>& tval) {
+static void transpose(Ctx& c, const BsrMat& X, DBuf<int>& trp, DBuf<int>& tci, DBuf<double>& tval, DBuf<int>& perm,
+                      DBuf<int>& rowof) {
   Scratch S(c);
   const long long nnz = X.nnzb;
-  int* row = S.get<int>(nnz);
+  perm.ensure(c.al, nnz);
+  rowof.ensure(c.al, nnz);
+  int* row = rowof.get();
   int* e0 = S.get<int>(nnz);
-  int* e1 = S.get<int>(nnz);
+  int* e1 = perm.get();
   int* kk = S.get<int>(nnz);
   k_row_of<<<grid_for(X.nbr), kThreads, 0, c.s>>>(X.nbr, X.rp, row, e0);
   SI_LAUNCHED(c);
@@ -2346,11 +2383,13 @@ static int aggregate_level(Ctx& c, Level& L, int lvl, const double* dnorm, Scrat
 template <int B, int K>
 static void build_transfer(Ctx& c, Level& L, Level& Lc, int lvl, int na, Scratch& S) {
   const int nb = L.nb;
-  // members sorted by aggregate (stable: node order inside an aggregate)
+  // members sorted by aggregate (stable: node order inside an aggregate); kept with the P_tent
+  // pattern for the numeric-only setup (reading G32)
   int* key = S.get<int>(nb);
   int* idx = S.get<int>(nb);
   int* skey = S.get<int>(nb);
-  int* members = S.get<int>(nb);
+  L.mem.ensure(c.al, nb);
+  int* members = L.mem.get();
   k_agg_key<<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.agg.get(), na, key, idx);
   SI_LAUNCHED(c);
   {
@@ -2363,19 +2402,24 @@ static void build_transfer(Ctx& c, Level& L, Level& Lc, int lvl, int na, Scratch
     SI_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, key, skey, idx, members, nb, 0, bits, c.s));
     c.launches += 2;
   }
-  int* start = S.get<int>(na + 1);
+  L.mstart.ensure(c.al, na + 1);
+  int* start = L.mstart.get();
   k_seg_starts<<<grid_for(na + 1), kThreads, 0, c.s>>>(na, nb, skey, start);
   SI_LAUNCHED(c);
   // P_tent pattern: one block per aggregated node
   int* f = S.get<int>(nb + 1);
-  int* ptrp = S.get<int>(nb + 1);
+  L.ptrp.ensure(c.al, nb + 1);
+  int* ptrp = L.ptrp.get();
   k_flag_agg<<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.agg.get(), f);
   SI_LAUNCHED(c);
   SI_CUDA(cudaMemsetAsync(f + nb, 0, sizeof(int), c.s));
   exclusive_scan(c, f, ptrp, nb + 1);
   const int ptn = read_scalar(c, ptrp + nb);
-  int* ptci = S.get<int>(ptn);
-  double* ptval = S.get<double>((size_t)ptn * B * K);
+  L.ptn = ptn;
+  L.ptci.ensure(c.al, ptn);
+  L.ptval.ensure(c.al, (size_t)ptn * B * K);
+  int* ptci = L.ptci.get();
+  double* ptval = L.ptval.get();
   k_ptent_ci<<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.agg.get(), ptrp, ptci);
   SI_LAUNCHED(c);
   Lc.B.ensure(c.al, (size_t)na * K * K);
@@ -2404,12 +2448,13 @@ static void build_transfer(Ctx& c, Level& L, Level& Lc, int lvl, int na, Scratch
                                                            L.Pci.get(), L.Pval.get());
       SI_LAUNCHED(c);
       fused = true;
+      L.plan[0] = SgPlan{};  // SG_NONE: the one-pass kernel
       tick(c, "A*Pt+smooth", lvl);
     }
   }
   if (!fused) {
     long long tn = 0;
-    spgemm<B, B, K>(c, view(L), Pt, L.Prp, L.Pci, L.Tval, tn);
+    spgemm<B, B, K>(c, view(L), Pt, L.Prp, L.Pci, L.Tval, tn, L.plan[0]);
     tick(c, "A*Pt", lvl);
     L.Pnnzb = tn;
     L.Pval.ensure(c.al, (size_t)tn * B * K);
@@ -2421,30 +2466,79 @@ static void build_transfer(Ctx& c, Level& L, Level& Lc, int lvl, int na, Scratch
   BsrMat P{nb, na, B, K, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.Pval.get()};
   tick(c, "smoothP", lvl);
   // R = P^T
-  transpose<B, K>(c, P, L.Rrp, L.Rci, L.Rval);
+  transpose<B, K>(c, P, L.Rrp, L.Rci, L.Rval, L.tperm, L.trow);
   L.Rnnzb = L.Pnnzb;
   tick(c, "transpose", lvl);
   BsrMat R{na, nb, K, B, L.Rnnzb, L.Rrp.get(), L.Rci.get(), L.Rval.get()};
   if (B == 2) {
     // finest level: A_c = (R A) P — the R A intermediate has one row per aggregate instead of
     // A P's one row per fine node and the product count halves (measured 37 -> 27 ms at n = 2048)
-    long long ran = 0;
-    spgemm<K, B, B>(c, R, view(L), c.ap_rp, c.ap_ci, c.ap_val, ran);
+    spgemm<K, B, B>(c, R, view(L), L.Irp, L.Ici, L.Ival, L.Innzb, L.plan[1]);
     tick(c, "R*A", lvl);
-    BsrMat RA{na, nb, K, B, ran, c.ap_rp.get(), c.ap_ci.get(), c.ap_val.get()};
-    spgemm<K, B, K>(c, RA, P, Lc.rp, Lc.ci, Lc.val, Lc.nnzb);
+    BsrMat RA{na, nb, K, B, L.Innzb, L.Irp.get(), L.Ici.get(), L.Ival.get()};
+    spgemm<K, B, K>(c, RA, P, Lc.rp, Lc.ci, Lc.val, Lc.nnzb, L.plan[2]);
     tick(c, "RA*P", lvl);
   } else {
     // coarse levels (wide rows): A_c = R (A P) measured faster
-    long long apn = 0;
-    spgemm<B, B, K>(c, view(L), P, c.ap_rp, c.ap_ci, c.ap_val, apn);
+    spgemm<B, B, K>(c, view(L), P, L.Irp, L.Ici, L.Ival, L.Innzb, L.plan[1]);
     tick(c, "A*P", lvl);
-    BsrMat AP{nb, na, B, K, apn, c.ap_rp.get(), c.ap_ci.get(), c.ap_val.get()};
-    spgemm<K, B, K>(c, R, AP, Lc.rp, Lc.ci, Lc.val, Lc.nnzb);
+    BsrMat AP{nb, na, B, K, L.Innzb, L.Irp.get(), L.Ici.get(), L.Ival.get()};
+    spgemm<K, B, K>(c, R, AP, Lc.rp, Lc.ci, Lc.val, Lc.nnzb, L.plan[2]);
     tick(c, "R*AP", lvl);
   }
   Lc.nb = na;
   Lc.b = K;
+  L.K = K;
+  k_fix_zero_diag<K><<<grid_for(na), kThreads, 0, c.s>>>(na, Lc.rp.get(), Lc.ci.get(), Lc.val.get());
+  SI_LAUNCHED(c);
+}
+
+// Numeric-only transfer of reading G32: the aggregates, every sparsity pattern and the SpGEMM
+// kernel choices of the last full setup are kept; the values are recomputed by the same kernels
+// (P_tent by MGS of the current near-nullspace, smoothed P with the current D^-1 and lambda,
+// R = P^T by the kept permutation, the Galerkin products on their kept patterns).
+template <int B, int K>
+static void build_transfer_numeric(Ctx& c, Level& L, Level& Lc, int lvl) {
+  const int nb = L.nb, na = L.nbc;
+  k_tentative_w<B, K><<<(int)(((long long)na * 32 + 127) / 128), 128, 0, c.s>>>(
+      na, L.mstart.get(), L.mem.get(), L.B.get(), L.ptrp.get(), L.ptval.get(), Lc.B.get());
+  SI_LAUNCHED(c);
+  tick(c, "tentative", lvl);
+  BsrMat Pt{nb, na, B, K, L.ptn, L.ptrp.get(), L.ptci.get(), L.ptval.get()};
+  const double omega = 4.0 / (3.0 * L.lmax);
+  if (L.plan[0].kind == SG_NONE) {
+    k_ptsm_fill<B, K><<<grid_for(nb, 128), 128, 0, c.s>>>(nb, L.rp.get(), L.ci.get(), L.val.get(), L.agg.get(),
+                                                         L.ptrp.get(), L.ptval.get(), L.dinv.get(), omega,
+                                                         L.Prp.get(), L.Pci.get(), L.Pval.get());
+    SI_LAUNCHED(c);
+  } else {
+    sg_numeric<B, B, K>(c, L.plan[0], view(L), Pt, L.Prp.get(), L.Pci.get(), L.Tval.get());
+    k_smooth_p<B, K><<<grid_for(nb), kThreads, 0, c.s>>>(nb, L.Prp.get(), L.Pci.get(), L.Tval.get(), L.dinv.get(),
+                                                      L.agg.get(), L.ptrp.get(), L.ptval.get(), omega, L.Pval.get());
+    SI_LAUNCHED(c);
+  }
+  tick(c, "smoothP", lvl);
+  if (L.Pnnzb > 0) {
+    k_transpose_gather<B, K><<<grid_for(L.Pnnzb), kThreads, 0, c.s>>>(L.Pnnzb, L.tperm.get(), L.trow.get(),
+                                                                     L.Pval.get(), L.Rci.get(), L.Rval.get());
+    SI_LAUNCHED(c);
+  }
+  tick(c, "transpose", lvl);
+  BsrMat P{nb, na, B, K, L.Pnnzb, L.Prp.get(), L.Pci.get(), L.Pval.get()};
+  BsrMat R{na, nb, K, B, L.Rnnzb, L.Rrp.get(), L.Rci.get(), L.Rval.get()};
+  if (B == 2) {
+    sg_numeric<K, B, B>(c, L.plan[1], R, view(L), L.Irp.get(), L.Ici.get(), L.Ival.get());
+    tick(c, "R*A", lvl);
+    BsrMat RA{na, nb, K, B, L.Innzb, L.Irp.get(), L.Ici.get(), L.Ival.get()};
+    sg_numeric<K, B, K>(c, L.plan[2], RA, P, Lc.rp.get(), Lc.ci.get(), Lc.val.get());
+    tick(c, "RA*P", lvl);
+  } else {
+    sg_numeric<B, B, K>(c, L.plan[1], view(L), P, L.Irp.get(), L.Ici.get(), L.Ival.get());
+    tick(c, "A*P", lvl);
+    BsrMat AP{nb, na, B, K, L.Innzb, L.Irp.get(), L.Ici.get(), L.Ival.get()};
+    sg_numeric<K, B, K>(c, L.plan[2], R, AP, Lc.rp.get(), Lc.ci.get(), Lc.val.get());
+    tick(c, "R*AP", lvl);
+  }
   k_fix_zero_diag<K><<<grid_for(na), kThreads, 0, c.s>>>(na, Lc.rp.get(), Lc.ci.get(), Lc.val.get());
   SI_LAUNCHED(c);
 }
@@ -2473,18 +2567,17 @@ void amg_free(Ctx& c) {
   c.vc_in.free_();
   c.vc_out.free_();
   for (auto& L : c.lv) {
-    DBuf<int>* ib[] = {&L.rp, &L.ci, &L.Prp, &L.Pci, &L.Rrp, &L.Rci, &L.agg};
-    DBuf<double>* db[] = {&L.val, &L.dinv, &L.Pval, &L.Rval, &L.B, &L.x, &L.rhs, &L.r, &L.d, &L.d2, &L.z, &L.Tval,
-                          &L.valT, &L.PvalT, &L.RvalT};
+    DBuf<int>* ib[] = {&L.rp,   &L.ci,   &L.Prp,  &L.Pci,   &L.Rrp,  &L.Rci, &L.agg, &L.mem,
+                       &L.mstart, &L.ptrp, &L.ptci, &L.tperm, &L.trow, &L.Irp, &L.Ici};
+    DBuf<double>* db[] = {&L.val,  &L.dinv, &L.Pval,  &L.Rval,  &L.B,     &L.x,     &L.rhs,   &L.r, &L.d,
+                          &L.d2,   &L.z,    &L.Tval,  &L.valT,  &L.PvalT, &L.RvalT, &L.ptval, &L.Ival};
     for (auto* b : ib) b->free_();
     for (auto* b : db) b->free_();
   }
   c.lv.clear();
   c.nlev = 0;
+  c.reuse_ok = false;
   c.cinv.free_();
-  c.ap_rp.free_();
-  c.ap_ci.free_();
-  c.ap_val.free_();
   c.arena.release_all(c.al);
   c.amg_ready = false;
 }
@@ -2507,11 +2600,23 @@ __global__ void k_level0_nullspace(int n, double L, int K, const double* __restr
 
 void vgraph_destroy(Ctx& c);
 
+static void amg_setup_numeric(Ctx& c, int K);
+
 void amg_setup_impl(Ctx& c) {
   SI_CHECK(c.assembled, SEAICE_ESTATE, "amg_setup before assemble");
   tick(c, nullptr, 0);
   vgraph_destroy(c);
   tick(c, "graph_free", 0);
+  int K = c.p.nullspace_dim;
+  SI_CHECK(K == 3 || c.lin_v.get(), SEAICE_ESTATE, "nullspace_dim = 4 needs an assembled linearisation point");
+  if (K == 4 && norm2(c, c.lin_v.get(), c.N) == 0.0) K = 3;  // reading G30: v_l = 0 adds no column
+  SI_CUDA(cudaMemsetAsync(c.flag.get(), 0, sizeof(int) * 4, c.s));
+  // reading G32: keep this time step's aggregates and patterns, recompute the values
+  c.last_setup_reused = c.p.amg_reuse == 1 && c.reuse_ok && c.reuse_K == K && c.nlev > 1;
+  if (c.last_setup_reused) {
+    amg_setup_numeric(c, K);
+    return;
+  }
   // the level pool keeps every buffer (grow-only) across setups; level 0's pattern is fixed
   if (c.lv.empty()) {
     c.lv.emplace_back();
@@ -2519,14 +2624,11 @@ void amg_setup_impl(Ctx& c) {
   }
   c.nlev = 1;
   c.amg_ready = false;
-  SI_CUDA(cudaMemsetAsync(c.flag.get(), 0, sizeof(int) * 4, c.s));
+  c.reuse_ok = false;
   Level& L0 = c.lv[0];
   L0.val.ensure(c.al, (size_t)L0.nnzb * 4);
   k_stencil_to_bsr<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L0.rp.get(), L0.val.get());
   SI_LAUNCHED(c);
-  int K = c.p.nullspace_dim;
-  SI_CHECK(K == 3 || c.lin_v.get(), SEAICE_ESTATE, "nullspace_dim = 4 needs an assembled linearisation point");
-  if (K == 4 && norm2(c, c.lin_v.get(), c.N) == 0.0) K = 3;  // reading G30: v_l = 0 adds no column
   L0.B.ensure(c.al, (size_t)c.Nn * 2 * K);
   k_level0_nullspace<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.p.L, K, c.lin_v.get(), L0.B.get());
   SI_LAUNCHED(c);
@@ -2589,6 +2691,59 @@ void amg_setup_impl(Ctx& c) {
   SI_CHECK(!(flag & 4), SEAICE_ENONFINITE, "AMG: singular diagonal block");
   SI_CHECK(!(flag & 8), SEAICE_ENONFINITE, "AMG: coarse matrix not positive definite");
   c.op_complexity = (double)nnz_total / (double)nnz0;
+  c.amg_ready = true;
+  c.reuse_ok = true;
+  c.reuse_K = K;
+  tick(c, "finish", c.nlev - 1);
+}
+
+// Reading G32: the hierarchy of the step's first setup with every value recomputed from the
+// current J and v_l (same level count, aggregates, patterns and kernels).
+static void amg_setup_numeric(Ctx& c, int K) {
+  c.amg_ready = false;
+  Level& L0 = c.lv[0];
+  k_stencil_to_bsr<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L0.rp.get(), L0.val.get());
+  SI_LAUNCHED(c);
+  k_level0_nullspace<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.p.L, K, c.lin_v.get(), L0.B.get());
+  SI_LAUNCHED(c);
+  tick(c, "to_bsr", 0);
+  for (int lvl = 0; lvl < c.nlev; ++lvl) {
+    Level& L = c.lv[lvl];
+    {
+      Scratch S(c);
+      double* dnorm = S.get<double>(L.nb);
+      if (L.b == 2) level_diag<2>(c, L, S, dnorm);
+      else if (L.b == 3) level_diag<3>(c, L, S, dnorm);
+      else level_diag<4>(c, L, S, dnorm);
+    }
+    tick(c, "diag", lvl);
+    if (lvl > 0 && L.b != 4) tile_copy(c, L.valT, L.val.get(), L.nnzb, L.b * L.b);
+    L.lmax = (L.b == 2) ? power_lambda<2>(c, L, lvl) : (L.b == 3) ? power_lambda<3>(c, L, lvl)
+                                                                  : power_lambda<4>(c, L, lvl);
+    tick(c, "power", lvl);
+    if (L.b == 3)  // V-cycle work vectors: pads stay 0 (as after a full setup)
+      for (auto* v : {&L.x, &L.rhs, &L.r, &L.d, &L.d2, &L.z})
+        SI_CUDA(cudaMemsetAsync(v->get(), 0, sizeof(double) * (size_t)L.nb * vstride(3), c.s));
+    if (lvl == c.nlev - 1) break;
+    Level& Lc = c.lv[lvl + 1];
+    if (K == 3) {
+      if (L.b == 2) build_transfer_numeric<2, 3>(c, L, Lc, lvl);
+      else build_transfer_numeric<3, 3>(c, L, Lc, lvl);
+    } else {
+      if (L.b == 2) build_transfer_numeric<2, 4>(c, L, Lc, lvl);
+      else build_transfer_numeric<4, 4>(c, L, Lc, lvl);
+    }
+    if (K != 4) {
+      tile_copy(c, L.PvalT, L.Pval.get(), L.Pnnzb, L.b * K);
+      tile_copy(c, L.RvalT, L.Rval.get(), L.Rnnzb, K * L.b);
+    }
+    tick(c, "tile_PR", lvl);
+  }
+  coarse_factor(c, c.lv[c.nlev - 1]);
+  tick(c, "coarse", c.nlev - 1);
+  const int flag = read_scalar(c, c.flag.get());
+  SI_CHECK(!(flag & 4), SEAICE_ENONFINITE, "AMG: singular diagonal block");
+  SI_CHECK(!(flag & 8), SEAICE_ENONFINITE, "AMG: coarse matrix not positive definite");
   c.amg_ready = true;
   tick(c, "finish", c.nlev - 1);
 }

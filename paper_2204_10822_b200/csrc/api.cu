@@ -72,8 +72,9 @@ void validate(const seaice_params* p) {
   SI_CHECK(p->krylov_forcing == 0 || p->krylov_forcing == 1, SEAICE_EINVAL, "krylov_forcing must be 0 or 1");
   SI_CHECK(p->nullspace_dim == 3 || p->nullspace_dim == 4, SEAICE_EINVAL, "nullspace_dim must be 3 or 4");
   SI_CHECK(p->krylov_method == 0 || p->krylov_method == 1, SEAICE_EINVAL, "krylov_method must be 0 or 1");
-  SI_CHECK(p->spgemm_path >= 0 && p->spgemm_path <= 5, SEAICE_EINVAL, "spgemm_path must be in 0..5");
+  SI_CHECK(p->spgemm_path >= 0 && p->spgemm_path <= 6, SEAICE_EINVAL, "spgemm_path must be in 0..6");
   SI_CHECK(p->amg_lag >= 0, SEAICE_EINVAL, "amg_lag must be >= 0");
+  SI_CHECK(p->amg_reuse == 0 || p->amg_reuse == 1, SEAICE_EINVAL, "amg_reuse must be 0 or 1");
 }
 
 int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* out) {
@@ -109,6 +110,7 @@ int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* o
     else amg_setup_impl(c);
     c.lag_ok = true;
     st.amg_rebuilt = lag ? 0 : 1;
+    st.amg_reused = (!lag && c.last_setup_reused) ? 1 : 0;
     st.t_amg = t.ms();
     st.amg_levels = c.nlev;
     st.amg_op_complexity = c.op_complexity;
@@ -222,6 +224,7 @@ int solve_step_impl(Ctx& c, double dt, double t_new, const double* h, const doub
     if (!ns.krylov.converged) st.krylov_capped++;
     st.krylov_max_iters = std::max(st.krylov_max_iters, ns.krylov.iters);
     st.amg_setups += ns.amg_rebuilt;
+    st.amg_reuses += ns.amg_reused;
     st.t_amg += ns.t_amg;
     st.t_krylov += ns.t_krylov;
     st.t_ls += ns.t_ls;
@@ -278,6 +281,7 @@ void seaice_default_params(seaice_params* p, int32_t n) {
   p->krylov_method = 0;
   p->spgemm_path = 0;
   p->amg_lag = 0;
+  p->amg_reuse = 0;
 }
 
 int seaice_create(const seaice_params* p, const seaice_runtime* rt, seaice_ctx** out) {

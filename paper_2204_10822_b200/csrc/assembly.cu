@@ -430,6 +430,7 @@ void set_step_impl(Ctx& c, double dt, double t_new, const double* h, const doubl
   c.amg_ready = false;
   c.have_r0 = false;
   c.lag_ok = false;  // a new time step starts with a full AMG setup (reading G31)
+  c.reuse_ok = false;  // ... and builds its own aggregates (reading G32)
   c.ew_prev_res = 0.0;
   c.ew_prev_eta = 0.0;
   c.ew_ls_failed = false;

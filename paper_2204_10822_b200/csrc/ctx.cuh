@@ -9,6 +9,15 @@
 
 namespace seaice {
 
+// Which numeric SpGEMM kernel produced a product (recorded by the full setup, replayed by the
+// numeric-only setup of reading G32; every path accumulates in the same order, so the choice
+// does not change the values).
+enum SgKind { SG_NONE = -1, SG_NARROW, SG_HASH1K, SG_HASH4K, SG_CTA, SG_THREAD, SG_GROUP8, SG_WARP };
+struct SgPlan {
+  int kind = SG_NONE;
+  size_t smem = 0;  // SG_CTA: dynamic shared memory of the launch
+};
+
 // One level of the AMG hierarchy.  Matrices are
 // block-CSR: A_l has b x b blocks (b = 2 on the finest level, 3 below), P_l has
 // b x 3 blocks, R_l = P_l^T has 3 x b blocks.
@@ -32,6 +41,15 @@ struct Level {
   // V-cycle copies of val / Pval / Rval in the chunk-of-32 SoA layout read by the group-per-row
   // kernels: element j of block e at ((e >> 5) * BB + j) * 32 + (e & 31)  (coalesced loads)
   DBuf<double> valT, PvalT, RvalT;
+  // kept for the numeric-only setup (reading G32): aggregate members sorted by aggregate and
+  // their segment starts, the P_tent pattern and values, the transpose permutation of P, the
+  // Galerkin intermediate (R A on the finest level, A P below) and the numeric kernel of each
+  // product (0: A P_tent, 1: the intermediate, 2: A_c)
+  DBuf<int> mem, mstart, ptrp, ptci, tperm, trow, Irp, Ici;
+  DBuf<double> ptval, Ival;
+  int ptn = 0, K = 0;
+  long long Innzb = 0;
+  SgPlan plan[3];
 };
 
 // Grow-only chunked bump allocator for setup scratch (LIFO marks): avoids an allocator
@@ -130,6 +148,9 @@ struct Ctx {
   std::string err;
   long long launches = 0;
   bool lag_ok = false;       // a hierarchy of this time step exists (amg_lag, reading G31)
+  bool reuse_ok = false;     // the hierarchy's aggregates were built in this time step (amg_reuse, G32)
+  int reuse_K = 0;           // its near-nullspace dimension
+  bool last_setup_reused = false;
   int last_krylov_its = 0;   // Krylov iterations of the previous Newton solve
   long long sg_hits[SEAICE_SPGEMM_PATHS] = {0, 0, 0, 0, 0, 0, 0};  // SpGEMM path counters (seaice_spgemm_path_hits)
 
@@ -172,8 +193,6 @@ struct Ctx {
   std::vector<Level> lv;
   int nlev = 0;
   Arena arena;
-  DBuf<int> ap_rp, ap_ci;
-  DBuf<double> ap_val;
   // the V-cycle as one CUDA graph (rebuilt after each setup): in vc_in -> out vc_out
   cudaGraphExec_t vgraph = nullptr;
   cudaStream_t cap_stream = nullptr;

@@ -37,7 +37,7 @@ class Params(C.Structure):
                 ("agg_dist", C.c_int32), ("cheb_fused", C.c_int32),
                 ("cheb_degree0", C.c_int32), ("matfree", C.c_int32),
                 ("krylov_forcing", C.c_int32), ("nullspace_dim", C.c_int32), ("krylov_method", C.c_int32),
-                ("spgemm_path", C.c_int32), ("amg_lag", C.c_int32)]
+                ("spgemm_path", C.c_int32), ("amg_lag", C.c_int32), ("amg_reuse", C.c_int32)]
 
 
 ALLOC_T = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -68,7 +68,7 @@ class NewtonStats(C.Structure):
                 ("alpha", C.c_double), ("dphi", C.c_double), ("halvings", C.c_int32), ("ls_stagnated", C.c_int32),
                 ("krylov", KrylovStats), ("amg_levels", C.c_int32), ("amg_op_complexity", C.c_double),
                 ("t_assemble", C.c_double), ("t_amg", C.c_double), ("t_krylov", C.c_double), ("t_ls", C.c_double),
-                ("amg_rebuilt", C.c_int32)]
+                ("amg_rebuilt", C.c_int32), ("amg_reused", C.c_int32)]
 
 
 class StepStats(C.Structure):
@@ -76,7 +76,7 @@ class StepStats(C.Structure):
                 ("res_norm0", C.c_double), ("res_norm_final", C.c_double), ("seconds", C.c_double),
                 ("t_assemble", C.c_double), ("t_amg", C.c_double), ("t_krylov", C.c_double), ("t_ls", C.c_double),
                 ("t_setup", C.c_double), ("krylov_solves", C.c_int32), ("krylov_capped", C.c_int32),
-                ("krylov_max_iters", C.c_int32), ("amg_setups", C.c_int32)]
+                ("krylov_max_iters", C.c_int32), ("amg_setups", C.c_int32), ("amg_reuses", C.c_int32)]
 
 
 def struct_dict(s):

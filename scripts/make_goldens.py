@@ -64,10 +64,13 @@ def run_cfg3(out):
     prm = wl.PhysParams()
     t0 = time.time()
     inp = wl.step_inputs(cfg, 0)
-    v, pi, h = newton.solve_step(inp, prm, linsolve="amg_fgmres")
+    # the AMG definition this golden was generated with (MIS(2) on every level: the oracle default
+    # before agg_dist = 3 became the coarse-level default); the GPU test runs the same definition
+    amg_params = {"agg_dist0": 2, "agg_dist": 2}
+    v, pi, h = newton.solve_step(inp, prm, linsolve="amg_fgmres", amg_params=amg_params)
     meta = {"config": 3, "n": cfg.n, "seed": cfg.seed, "step": 1,
             "solver": "oracle sv-Newton, AMG-FGMRES(30) rtol 1e-8 (oracle/amg.py defaults: nullspace_dim 4, reading G30)",
-            "gpu_params": {},
+            "gpu_params": dict(amg_params), "amg_params": amg_params,
             "newton": h["newton_iters"], "converged": bool(h["converged"]), "relres": h["res"][-1] / h["res"][0],
             "krylov": [k["iters"] for k in h["krylov"]], "levels": [k.get("levels") for k in h["krylov"]],
             "alphas": h["alpha"], "res": h["res"], "seconds": round(time.time() - t0, 1),

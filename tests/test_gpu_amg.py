@@ -259,11 +259,12 @@ def _plastic_state(n, seed):
     return inp, pb, v, pb.pi_consistent(v)
 
 
-@pytest.mark.parametrize("n,path", [(256, 0), (512, 0), (256, 1), (256, 2), (256, 3), (256, 4), (256, 5)])
+@pytest.mark.parametrize("n,path", [(256, 0), (512, 0), (256, 1), (256, 2), (256, 3), (256, 4), (256, 5),
+                                    (256, 6)])
 def test_hierarchy_matches_oracle_at_scale(n, path):
     """AMG hierarchy parity at sizes that take the SpGEMM code paths config 4 uses (verdict r1):
     same level count, identical aggregates, A_l and P_l to 1e-11 row-relative, with the automatic
-    path choice (path 0) and with every product forced through each SpGEMM path (1-4); the set
+    path choice (path 0) and with every product forced through each SpGEMM path (1-6); the set
     of paths config 4 (n = 2048) takes is then covered by the paths exercised here."""
     inp, pb, v, pi = _plastic_state(n, 21)
     J = pb.jacobian(v, pi, "sv")
@@ -294,7 +295,7 @@ def test_config4_spgemm_paths_are_parity_covered():
     """Runs after test_hierarchy_matches_oracle_at_scale (file order): the paths config 4's setup
     takes (a plastic state and a late Newton iterate of its first step) are all among those the
     n = 256 / 512 parity cases exercised."""
-    if len(_covered) < 7:
+    if len(_covered) < 8:
         pytest.skip("needs test_hierarchy_matches_oracle_at_scale in the same session")
     covered = set().union(*_covered.values())
     cfg = wl.CONFIGS[4]
@@ -355,4 +356,64 @@ def test_newton_ew_lagged_hierarchy_matches_oracle(n, lag):
         assert abs(st["amg_setups"] - so) <= 1, (s, st["amg_setups"], so)
         if lag == 0:
             assert st["amg_setups"] == st["newton_iters"]
+        assert np.linalg.norm(np_(vg) - vo_) <= 1e-8 * np.linalg.norm(vo_), s
+
+
+@pytest.mark.parametrize("n", [64, 256])
+def test_reused_hierarchy_matches_oracle(n):
+    """Reading G32 (amg_reuse = 1): a setup after a full setup in the same time step keeps the
+    aggregates and every pattern and recomputes the values (numeric-only SpGEMMs on the kept
+    patterns and kernel choices).  Against oracle amg.setup(J2, v=v2, reuse=H1): same levels,
+    identical aggregates, A_l and P_l to 1e-11 row-relative, and the same V-cycle."""
+    inp, pb, v1, pi1 = _plastic_state(n, 31)
+    v2 = 0.7 * v1 + wl.random_velocity(n, 33, amp=0.02)
+    pi2 = pb.pi_consistent(v2)
+    J1 = pb.jacobian(v1, pi1, "sv")
+    J2 = pb.jacobian(v2, pi2, "sv")
+    H1 = OA.setup(J1, pb, v=v1)
+    H2 = OA.setup(J2, pb, v=v2, reuse=H1)
+    assert H2["reused"]
+    ctx = make_ctx(n, amg_reuse=1)
+    ctx.set_inputs(inp)
+    ctx.assemble_jacobian(v1, pi1.ravel(), want_csr=False)
+    ctx.amg_setup()
+    hits0 = sum(ctx.spgemm_path_hits())
+    ctx.assemble_jacobian(v2, pi2.ravel(), want_csr=False)
+    nlev, _ = ctx.amg_setup()
+    assert sum(ctx.spgemm_path_hits()) == hits0  # no symbolic SpGEMM ran: the patterns were kept
+    assert nlev == len(H2["levels"])
+    for l in range(nlev):
+        A, P, agg = ctx.amg_level(l)
+        assert rows_close(bsr_to_scipy(A), H2["levels"][l]["A"], 1.0) <= 1e-11, l
+        if l < nlev - 1:
+            assert np.array_equal(agg, H1["levels"][l]["agg"]), l
+            assert rows_close(bsr_to_scipy(P), H2["levels"][l]["P"], 1.0) <= 1e-11, l
+    # the V-cycle built on the reused hierarchy is the oracle's
+    r = wl.random_interior_vector(n, 8)
+    zo = OA.vcycle(H2, r)
+    zg = np_(ctx.precond_apply(r))
+    assert np.linalg.norm(zg - zo) <= 1e-9 * np.linalg.norm(zo)
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_newton_ew_reused_aggregates_matches_oracle(n):
+    """Product path with amg_reuse = 1 (reading G32) and Eisenstat-Walker forcing over two
+    moving-cyclone steps: Newton count (+-1), Krylov total (+-10 %), the number of setups that
+    kept the aggregates (+-1) and the converged velocity (1e-8) match oracle tier B."""
+    cfg = wl.Config(f"reuse{n}", n, 2, 2, True)
+    hA = wl.ice_fields(cfg)
+    ctx = make_ctx(n, krylov_forcing=1, amg_reuse=1)
+    vo_ = None
+    vg = torch.zeros(ctx.N, dtype=torch.float64, device="cuda")
+    for s in range(2):
+        inp = wl.step_inputs(cfg, s, v_prev=vo_, h_A=hA)
+        vo_, _, ho = newton.solve_step(inp, PRM, linsolve="amg_fgmres", forcing=1, amg_reuse=1)
+        vin = vg.clone()
+        vg, st = ctx.solve_step(inp.dt, inp.t_new, inp.h, inp.A, vin, inp.v_air, inp.v_ocean)
+        assert st["converged"] == 1 and ho["converged"], (s, st)
+        assert abs(st["newton_iters"] - ho["newton_iters"]) <= 1, (s, st["newton_iters"], ho["newton_iters"])
+        ko = sum(k["iters"] for k in ho["krylov"])
+        assert abs(st["krylov_iters_total"] - ko) <= 0.1 * ko + 2, (s, st["krylov_iters_total"], ko)
+        ro = sum(ho["amg_reused"])
+        assert abs(st["amg_reuses"] - ro) <= 1 and st["amg_reuses"] >= st["newton_iters"] - 2, (s, st, ro)
         assert np.linalg.norm(np_(vg) - vo_) <= 1e-8 * np.linalg.norm(vo_), s

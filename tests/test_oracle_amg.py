@@ -237,3 +237,51 @@ def test_misd_is_distance_d_independent_and_maximal(dist):
     assert np.all(sub.row == sub.col), f"two roots within distance {dist}"
     covered = np.asarray(Cd[:, R].sum(axis=1)).ravel() > 0
     assert np.all(covered | isolated)
+
+
+def test_reused_aggregates_hierarchy_is_galerkin_for_the_new_operator():
+    """Reading G32 (amg.setup(..., reuse=H)): with the aggregates of a hierarchy built for one
+    (J1, v1), the hierarchy for another (J2, v2) keeps every level's aggregates and the level
+    count, its tentative prolongators reproduce the NEW near-nullspace [rigid modes, v2] exactly,
+    its coarse operators are P^T A P of the new operator (checked densely, not through the
+    oracle's own product order), and reusing a hierarchy's own aggregates reproduces it."""
+    n = 20
+    _, inp = wl.custom_inputs(n, seed=5)
+    pb = M.Problem(inp, PRM)
+    v1 = wl.random_velocity(n, 6, amp=0.05)
+    v2 = wl.random_velocity(n, 9, amp=0.03)
+    J1 = pb.jacobian(v1, pb.pi_consistent(v1), "sv").tocsr()
+    J2 = pb.jacobian(v2, pb.pi_consistent(v2), "sv").tocsr()
+    H1 = amg.setup(J1, pb, v=v1, coarse_max_dof=60)
+    H2 = amg.setup(J2, pb, v=v2, coarse_max_dof=60, reuse=H1)
+    assert H2["reused"] and len(H2["levels"]) == len(H1["levels"]) >= 3
+    Bl = amg.level0_nullspace(n, pb.L, v2)
+    b = 2
+    for l1, l2 in zip(H1["levels"][:-1], H2["levels"][:-1]):
+        assert np.array_equal(l1["agg"], l2["agg"])
+        Pt = l2["Ptent"].toarray()
+        rows = np.repeat(l2["agg"] >= 0, b)  # isolated rows are zero rows of P_tent
+        # P_tent has orthonormal columns and spans the level's (new) near-nullspace on aggregated rows
+        PtP = Pt.T @ Pt
+        keep = np.diag(PtP) > 0.5
+        assert np.allclose(PtP[np.ix_(keep, keep)], np.eye(keep.sum()), atol=1e-12)
+        coef, *_ = np.linalg.lstsq(Pt[rows], Bl[rows], rcond=None)
+        assert np.linalg.norm(Pt[rows] @ coef - Bl[rows]) <= 1e-10 * np.linalg.norm(Bl[rows])
+        Bl, b = coef, Bl.shape[1]
+    for l, lev in enumerate(H2["levels"][:-1]):
+        A = lev["A"].toarray()
+        P = lev["P"].toarray()
+        Ac = H2["levels"][l + 1]["A"].toarray()
+        d = np.diag(Ac).copy()
+        ref = P.T @ A @ P
+        fix = np.diag(ref) == 0.0
+        ref[np.diag_indices_from(ref)] += fix.astype(float)
+        assert np.abs(Ac - ref).max() <= 1e-10 * np.abs(ref).max(), l
+        assert np.all(d > 0)
+    assert np.abs(H2["levels"][0]["A"] - J2).max() == 0.0
+    H1b = amg.setup(J1, pb, v=v1, coarse_max_dof=60, reuse=H1)
+    for a, b in zip(H1["levels"], H1b["levels"]):
+        assert abs(a["A"] - b["A"]).max() == 0.0 and a["lmax"] == b["lmax"]
+    # a different near-nullspace dimension falls back to a full setup
+    H3 = amg.setup(J2, pb, v=np.zeros_like(v2), coarse_max_dof=60, reuse=H1)
+    assert not H3["reused"]

@@ -83,8 +83,12 @@ typedef struct {
   int32_t agg_dist0;       /* aggregation root distance on the finest level: 2 = MIS(2) (default), 1 = MIS(1),
                               3 = MIS(3) (larger aggregates) */
   int32_t agg_dist;        /* same on coarse levels (default 3) */
-  int32_t cheb_fused;      /* 1 (default): finest-level Chebyshev(3) as one temporally blocked launch
-                              (same arithmetic per node and step); 0: one launch per step */
+  int32_t cheb_fused;      /* finest-level Chebyshev(3): 2 (default) one y-streamed, TMA-fed temporally
+                              blocked launch per smoothing (the post-smoothing residual included; reads a
+                              tensor-map copy of the stencil, vectors must be 16-byte aligned); 1: one
+                              tile-blocked launch (+ a residual launch for post-smoothing); 0: one launch
+                              per step.  Same arithmetic per node and step (A u summed in another order
+                              for 2) */
   int32_t cheb_degree0;    /* Chebyshev degree on the finest level (0: cheb_degree) */
   int32_t matfree;         /* 0 (default): FGMRES applies the assembled stencil J; 1: FGMRES applies
                               J(v, pi) matrix-free from the (v, pi) of the

@@ -9,6 +9,7 @@
 // CUB's stable radix / segmented sorts, SpGEMM accumulates each output block in a fixed
 // (row-major product) order by a single thread, reductions are fixed-order two-stage.
 #include <cub/cub.cuh>
+#include <cuda.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1740,6 +1741,335 @@ static void launch_chebM(Ctx& c, const double* dinv, const double* rin, const do
   else launch_chebM_t<M, 4>(c, dinv, rin, d0g, rout, x, kc, pre);
 }
 
+// Chebyshev(3) smoothing on the stencil level as a y-streamed (sliding-window) temporally
+// blocked launch fed by TMA (cheb_fused = 2).  A CTA owns a strip of kTTX = 60 node columns
+// (64 threads wide with the 2 + 2 ring columns of steps 1 and 2: two warps per node row) and a
+// segment of rows [ja, jb); it walks the rows in ticks, one __syncthreads per tick.
+//   * One elected thread streams the rows into a kTNS-slot shared-memory ring with tensor-map
+//     bulk copies (cp.async.bulk.tensor, completion on one mbarrier per slot): the stencil row
+//     block of the smoother copy Jsm[j][e][x] (68 x 20 doubles), Dinv, b and (post) x_0 on 66
+//     columns.  ~10 rows (150 KB) per SM are in flight, independent of the compute warps, and
+//     out-of-domain rows / columns arrive as zeros (no boundary branches: a Dirichlet row of the
+//     symmetric storage is the identity row, an out-of-domain row is zero).
+//   * Warp pair p owns the rows r = rho(p) + 8 m of the segment.  Its row program takes 8
+//     ticks: stage 0 (wait for the slot, stencil row -> registers incl. the transposed upper
+//     blocks of the lower neighbours from this and the previous slot, u0 -> shared), the TMA
+//     issue for the slot it just released, then stages 1, 2, 3 two ticks apart (stage k of
+//     row j reads u_{k-1} of rows j - 1, j, j + 1 from an 8-row shared ring).  The 8 pairs are
+//     in 8 different phases: loads, the four stages and the stores of different rows overlap;
+//     there are no ring rows (60 of 64 threads produce output; the tile kernel: 336 of 512).
+// Arithmetic per node and step is that of k_chebM_stencil up to the summation order of A u:
+//   PRE  (x_0 = 0):  u0 = d_0 = ith Dinv b;  stage k: r -= A u_{k-1}, x += u_{k-1},
+//                    u_k = c1 u_{k-1} + c2 Dinv r;  writes x_3 and r_3.
+//   POST (x_0 = xin): u0 = x_0;  stage 1: r = b - A x_0, u1 = d_0 = ith Dinv r;  stages 2, 3 as
+//                    above (d_1, d_2);  writes x_0 + d_0 + d_1 + d_2 to xout != xin (ring columns
+//                    and rows of x_0 belong to other CTAs' outputs).  The residual pass
+//                    k_resid_dinv_stencil of the tile path is part of the launch.
+constexpr int kTW = 64, kTTX = 60, kTNP = 8, kTNS = 12, kTBX = 68, kTHX = 66, kTJE = 20;
+constexpr int kTOffD = kTBX * kTJE * 8;                         // 10880 (multiple of 128)
+constexpr int kTOffB = (kTOffD + kTHX * 32 + 127) / 128 * 128;  // 13056
+constexpr int kTOffX = (kTOffB + kTHX * 16 + 127) / 128 * 128;  // 14208
+constexpr int kTSlot = (kTOffX + kTHX * 16 + 127) / 128 * 128;  // 15360
+constexpr int kTSuBytes = 3 * kTNP * kTHX * 16;
+constexpr int kTSmem = kTNS * kTSlot + kTSuBytes + kTNS * 8;
+static_assert(kTOffD % 128 == 0 && kTSmem <= 227 * 1024, "streamed smoother shared-memory layout");
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// A u at this thread's node: stencil row in registers, u rows from the shared ring; three partial
+// sums per component (one per stencil row) keep the dependent-DFMA chains short
+__device__ __forceinline__ double2 stream_apply(const double (&Jr)[36], const double2* __restrict__ rm,
+                                                const double2* __restrict__ r0, const double2* __restrict__ rp,
+                                                int c) {
+  double a0[3], a1[3];
+#pragma unroll
+  for (int rr = 0; rr < 3; ++rr) {
+    const double2* row = rr == 0 ? rm : (rr == 1 ? r0 : rp);
+    const double2 vm = row[c - 1], v0 = row[c], vp = row[c + 1];
+    const int sl = rr * 3;
+    a0[rr] = Jr[sl * 4 + 0] * vm.x + Jr[sl * 4 + 1] * vm.y;
+    a1[rr] = Jr[sl * 4 + 2] * vm.x + Jr[sl * 4 + 3] * vm.y;
+    a0[rr] += Jr[sl * 4 + 4] * v0.x + Jr[sl * 4 + 5] * v0.y;
+    a1[rr] += Jr[sl * 4 + 6] * v0.x + Jr[sl * 4 + 7] * v0.y;
+    a0[rr] += Jr[sl * 4 + 8] * vp.x + Jr[sl * 4 + 9] * vp.y;
+    a1[rr] += Jr[sl * 4 + 10] * vp.x + Jr[sl * 4 + 11] * vp.y;
+  }
+  return make_double2((a0[0] + a0[1]) + a0[2], (a1[0] + a1[1]) + a1[2]);
+}
+
+// Smoother copy of the stencil: Jsm[(j * 20 + e) * sp + x] = Jst[e * Nn + j * s + x] (sp = row
+// pitch, even, so every (j, e) line is 16-byte aligned for the tensor map); plane 19 and the pad
+// columns stay zero.
+__global__ void k_stencil_to_stream(int s, int sp, long long Nn, const double* __restrict__ Jst,
+                                    double* __restrict__ Jsm) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (x >= s) return;
+  const long long node = (long long)j * s + x;
+#pragma unroll
+  for (int e = 0; e < kJS; ++e) Jsm[((long long)j * kTJE + e) * sp + x] = Jst[e * Nn + node];
+}
+
+template <bool PRE>
+__global__ void __launch_bounds__(kTNP * 64, 1)
+    k_cheb3_stream(const __grid_constant__ CUtensorMap tmJ, const __grid_constant__ CUtensorMap tmD,
+                   const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX, int n,
+                   int seg_rows, double2* __restrict__ xout, double2* __restrict__ rout, ChebFCoef k) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  typedef double2 URow[kTHX];
+  URow* su = reinterpret_cast<URow*>(smem + kTNS * kTSlot);  // su[k * kTNP + q][col]
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem + kTNS * kTSlot + kTSuBytes);
+  const int s = n + 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, p = w >> 1, hf = w & 1;
+  // rows 2 ticks apart (the compute stages of one tick) alternate between the two scheduler pairs
+  const int rho = 2 * (p & 1) + ((p >> 1) & 1) + 4 * (p >> 2);
+  const int i0 = blockIdx.x * kTTX, ja = blockIdx.y * seg_rows;
+  const int jb = min(ja + seg_rows, s);
+  const int jbase = ja - 3, nrows = jb + 3 - jbase;
+  const int cidx = hf * 32 + lane, gi = i0 - 2 + cidx;
+  const int di = cidx < 2 ? 2 - cidx : (cidx >= kTTX + 2 ? cidx - (kTTX + 1) : 0);
+  const bool col_in = gi >= 0 && gi <= n;
+  const int c = cidx + 1;  // column in the 66-wide u / Dinv / b / x rows
+  constexpr unsigned kBytes = kTBX * kTJE * 8 + kTHX * 32 + kTHX * 16 + (PRE ? 0 : kTHX * 16);
+  auto issue = [&](int r) {  // one thread: stream row jbase + r into its slot
+    const int slot = r % kTNS, j = jbase + r;
+    unsigned char* dst = smem + slot * kTSlot;
+    mbar_expect_tx(&mbar[slot], kBytes);
+    tma_load_3d(dst, &tmJ, i0 - 4, 0, j, &mbar[slot]);
+    tma_load_3d(dst + kTOffD, &tmD, 0, i0 - 3, j, &mbar[slot]);
+    tma_load_3d(dst + kTOffB, &tmB, 0, i0 - 3, j, &mbar[slot]);
+    if (!PRE) tma_load_3d(dst + kTOffX, &tmX, 0, i0 - 3, j, &mbar[slot]);
+  };
+  if (threadIdx.x == 0) {
+    for (int sl = 0; sl < kTNS; ++sl) mbar_init(&mbar[sl], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int r = 0; r < kTNS - 1 && r < nrows; ++r) issue(r);
+  }
+  __syncthreads();
+  const int nticks = nrows + kTNP - 1;
+  // every warp executes one barrier per tick, at the point of its own row program
+  int done = rho;
+  for (int t = 0; t < rho; ++t) __syncthreads();
+  for (int r = rho; r < nrows; r += kTNP, done += kTNP) {
+    const int j = jbase + r, slot = r % kTNS, pslot = (r + kTNS - 1) % kTNS;
+    const int q = r & (kTNP - 1), qm = (q - 1) & (kTNP - 1), qp = (q + 1) & (kTNP - 1);
+    const int node = j * s + gi;
+    double Jr[36];
+    double2 rv, xa = make_double2(0.0, 0.0);
+    double4 D;
+    {  // tick r, stage 0: this row's data -> registers, u0 -> shared
+      mbar_wait(&mbar[slot], (r / kTNS) & 1);
+      if (r > 0) mbar_wait(&mbar[pslot], ((r - 1) / kTNS) & 1);  // row j-1's copy (completed a tick ago)
+      const double* Js = reinterpret_cast<const double*>(smem + slot * kTSlot) + (cidx + 2);
+      const double* Jm = reinterpret_cast<const double*>(smem + pslot * kTSlot) + (cidx + 2);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) Jr[(5 + u) * 4 + e] = Js[(4 * u + e) * kTBX];
+        // lower half: transposed upper block u of the neighbour at -off_u (W: this row, x-1;
+        // SE, S, SW: row j-1 at x+1, x, x-1)
+        const double* lo = (u == 0 ? Js - 1 : Jm + (2 - u)) + 4 * u * kTBX;
+        const int sl = 3 - u;
+        Jr[sl * 4 + 0] = lo[0];
+        Jr[sl * 4 + 1] = lo[2 * kTBX];
+        Jr[sl * 4 + 2] = lo[kTBX];
+        Jr[sl * 4 + 3] = lo[3 * kTBX];
+      }
+      Jr[16] = Js[kJDxx * kTBX];
+      Jr[17] = Js[kJDxy * kTBX];
+      Jr[18] = Jr[17];
+      Jr[19] = Js[kJDyy * kTBX];
+      const unsigned char* sb = smem + slot * kTSlot;
+      const double4* Ds = reinterpret_cast<const double4*>(sb + kTOffD);
+      const double2* bs = reinterpret_cast<const double2*>(sb + kTOffB);
+      const double2* xs = reinterpret_cast<const double2*>(sb + kTOffX);
+      D = Ds[c];
+      rv = bs[c];
+      double2 u0;
+      if (PRE) {
+        u0 = make_double2(k.ith * (D.x * rv.x + D.y * rv.y), k.ith * (D.z * rv.x + D.w * rv.y));
+      } else {
+        xa = xs[c];
+        u0 = xa;
+      }
+      su[q][c] = u0;
+      if (cidx == 0 || cidx == kTW - 1) {  // 3rd-ring columns of u0
+        const int hc = cidx == 0 ? 0 : kTHX - 1;
+        if (PRE) {
+          const double4 hD = Ds[hc];
+          const double2 hb = bs[hc];
+          su[q][hc] = make_double2(k.ith * (hD.x * hb.x + hD.y * hb.y), k.ith * (hD.z * hb.x + hD.w * hb.y));
+        } else {
+          su[q][hc] = xs[hc];
+        }
+      }
+    }
+    __syncthreads();
+    // tick r + 1: the slot of row j-1 was last read in tick r (by this pair): refill it
+    if (hf == 0 && lane == 0 && r + kTNS - 1 < nrows) issue(r + kTNS - 1);
+    __syncthreads();
+    // tick r + 2, stage 1 (rows ja-2 .. jb+1, all 64 columns)
+    if (j >= ja - 2 && j < jb + 2) {
+      const double2 y = stream_apply(Jr, su[qm], su[q], su[qp], c);
+      rv.x -= y.x;
+      rv.y -= y.y;
+      const double z0 = D.x * rv.x + D.y * rv.y, z1 = D.z * rv.x + D.w * rv.y;
+      if (PRE) {
+        const double2 dv = su[q][c];
+        xa = dv;
+        su[kTNP + q][c] = make_double2(k.c1[0] * dv.x + k.c2[0] * z0, k.c1[0] * dv.y + k.c2[0] * z1);
+      } else {
+        su[kTNP + q][c] = make_double2(k.ith * z0, k.ith * z1);
+      }
+    }
+    __syncthreads();
+    __syncthreads();
+    // tick r + 4, stage 2 (rows ja-1 .. jb, ring depth <= 1)
+    if (di <= 1 && j >= ja - 1 && j < jb + 1) {
+      const double2 dv = su[kTNP + q][c];
+      const double2 y = stream_apply(Jr, su[kTNP + qm], su[kTNP + q], su[kTNP + qp], c);
+      rv.x -= y.x;
+      rv.y -= y.y;
+      xa.x += dv.x;
+      xa.y += dv.y;
+      const double z0 = D.x * rv.x + D.y * rv.y, z1 = D.z * rv.x + D.w * rv.y;
+      constexpr int ci = PRE ? 1 : 0;
+      su[2 * kTNP + q][c] = make_double2(k.c1[ci] * dv.x + k.c2[ci] * z0, k.c1[ci] * dv.y + k.c2[ci] * z1);
+    }
+    __syncthreads();
+    __syncthreads();
+    // tick r + 6, stage 3 (rows ja .. jb-1, strip columns)
+    if (di == 0 && col_in && j >= ja && j < jb) {
+      const double2 dv = su[2 * kTNP + q][c];
+      xa.x += dv.x;
+      xa.y += dv.y;
+      const double2 y = stream_apply(Jr, su[2 * kTNP + qm], su[2 * kTNP + q], su[2 * kTNP + qp], c);
+      rv.x -= y.x;
+      rv.y -= y.y;
+      if (PRE) {
+        xout[node] = xa;
+        rout[node] = rv;
+      } else {
+        const double z0 = D.x * rv.x + D.y * rv.y, z1 = D.z * rv.x + D.w * rv.y;
+        xa.x += k.c1[1] * dv.x + k.c2[1] * z0;
+        xa.y += k.c1[1] * dv.y + k.c2[1] * z1;
+        xout[node] = xa;
+      }
+    }
+    __syncthreads();
+    __syncthreads();  // tick r + 7: idle
+  }
+  for (; done < nticks; ++done) __syncthreads();
+}
+
+// segments per strip so that the grid fills the SMs (1 CTA per SM) in whole waves
+static int stream_segments(int strips, int rows, int sms) {
+  int best = 1;
+  double best_eff = 0.0;
+  for (int g = 1; g <= 64; ++g) {
+    const int seg = (rows + g - 1) / g;
+    if (g > 1 && seg < 48) break;
+    const int ctas = strips * ((rows + seg - 1) / seg);
+    const int waves = (ctas + sms - 1) / sms;
+    // per-CTA time ~ seg + pipeline fill; efficiency = useful row-ticks / (waves * sms * ticks per CTA)
+    const double eff = (double)strips * rows / ((double)waves * sms * (seg + 6 + kTNP));
+    if (eff > best_eff * 1.02) {
+      best_eff = eff;
+      best = g;
+    }
+  }
+  return best;
+}
+
+typedef CUresult (*TmapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static TmapEncodeFn tmap_encode_fn() {
+  static TmapEncodeFn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    SI_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr));
+    SI_CHECK(f && qr == cudaDriverEntryPointSuccess, SEAICE_ESTATE, "cuTensorMapEncodeTiled not available");
+    fn = (TmapEncodeFn)f;
+  }
+  return fn;
+}
+// fp64 rank-3 tiled tensor map (dims innermost first, strides in bytes for dims 1 and 2)
+static CUtensorMap tmap3(const void* base, cuuint64_t d0, cuuint64_t d1, cuuint64_t d2, cuuint64_t st1,
+                         cuuint64_t st2, cuuint32_t b0, cuuint32_t b1) {
+  SI_CHECK((reinterpret_cast<uintptr_t>(base) & 15) == 0, SEAICE_EINVAL,
+           "streamed smoother: vectors must be 16-byte aligned");
+  CUtensorMap tm;
+  const cuuint64_t dims[3] = {d0, d1, d2}, strides[2] = {st1, st2};
+  const cuuint32_t box[3] = {b0, b1, 1}, es[3] = {1, 1, 1};
+  const CUresult r = tmap_encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides,
+                                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SI_CHECK(r == CUDA_SUCCESS, SEAICE_ESTATE, "cuTensorMapEncodeTiled failed");
+  return tm;
+}
+
+// (re)build the smoother copy of the finest stencil from Jst (after every assembly that the
+// hierarchy's finest level is refreshed from)
+static void stencil_stream_copy(Ctx& c) {
+  const int s = c.n + 1, sp = (s + 1) & ~1;
+  const size_t len = (size_t)s * kTJE * sp;
+  if (c.Jsm.cap < len) {
+    c.Jsm.ensure(c.al, len);
+    SI_CUDA(cudaMemsetAsync(c.Jsm.get(), 0, len * sizeof(double), c.s));
+  }
+  k_stencil_to_stream<<<dim3((s + 255) / 256, s), 256, 0, c.s>>>(s, sp, c.Nn, c.Jst.get(), c.Jsm.get());
+  SI_LAUNCHED(c);
+}
+
+static void launch_cheb3_stream(Ctx& c, const double* dinv, const double* b, const double* xin, double* xout,
+                                double* rout, const ChebFCoef& kc, bool pre) {
+  const int s = c.n + 1, sp = (s + 1) & ~1, strips = (s + kTTX - 1) / kTTX;
+  static const int seg_env = getenv("SEAICE_CHEB_SEGS") ? atoi(getenv("SEAICE_CHEB_SEGS")) : 0;  // tuning aid
+  const int g = seg_env > 0 ? seg_env : stream_segments(strips, s, c.sms);
+  const int seg = (s + g - 1) / g;
+  const dim3 grid(strips, (s + seg - 1) / seg);
+  const CUtensorMap tmJ = tmap3(c.Jsm.get(), sp, kTJE, s, 8ull * sp, 8ull * sp * kTJE, kTBX, kTJE);
+  const CUtensorMap tmD = tmap3(dinv, 4, s, s, 32, 32ull * s, 4, kTHX);
+  const CUtensorMap tmB = tmap3(b, 2, s, s, 16, 16ull * s, 2, kTHX);
+  const CUtensorMap tmX = pre ? tmB : tmap3(xin, 2, s, s, 16, 16ull * s, 2, kTHX);
+  static bool attr = false;
+  if (!attr) {
+    SI_CUDA(cudaFuncSetAttribute(k_cheb3_stream<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem));
+    SI_CUDA(cudaFuncSetAttribute(k_cheb3_stream<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem));
+    attr = true;
+  }
+  if (pre)
+    k_cheb3_stream<true><<<grid, kTNP * 64, kTSmem, c.s>>>(tmJ, tmD, tmB, tmX, c.n, seg, (double2*)xout, (double2*)rout, kc);
+  else
+    k_cheb3_stream<false><<<grid, kTNP * 64, kTSmem, c.s>>>(tmJ, tmD, tmB, tmX, c.n, seg, (double2*)xout, nullptr, kc);
+}
+
 // r = b - A x (or r = b if x == NULL); d = Dinv r * c2 (stencil level)
 __global__ void __launch_bounds__(256) k_resid_dinv_stencil(int n, int Nn, const double* __restrict__ J,
                                                             const double* __restrict__ dinv,
@@ -2629,6 +2959,7 @@ void amg_setup_impl(Ctx& c) {
   L0.val.ensure(c.al, (size_t)L0.nnzb * 4);
   k_stencil_to_bsr<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L0.rp.get(), L0.val.get());
   SI_LAUNCHED(c);
+  if (c.p.cheb_fused == 2) stencil_stream_copy(c);
   L0.B.ensure(c.al, (size_t)c.Nn * 2 * K);
   k_level0_nullspace<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.p.L, K, c.lin_v.get(), L0.B.get());
   SI_LAUNCHED(c);
@@ -2704,6 +3035,7 @@ static void amg_setup_numeric(Ctx& c, int K) {
   Level& L0 = c.lv[0];
   k_stencil_to_bsr<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L0.rp.get(), L0.val.get());
   SI_LAUNCHED(c);
+  if (c.p.cheb_fused == 2) stencil_stream_copy(c);
   k_level0_nullspace<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.p.L, K, c.lin_v.get(), L0.B.get());
   SI_LAUNCHED(c);
   tick(c, "to_bsr", 0);
@@ -2758,6 +3090,7 @@ void amg_refresh_finest(Ctx& c) {
   Level& L0 = c.lv[0];
   k_stencil_to_bsr<<<grid_for(c.Nn), kThreads, 0, c.s>>>(c.n, c.Nn, c.Jst.get(), L0.rp.get(), L0.val.get());
   SI_LAUNCHED(c);
+  if (c.p.cheb_fused == 2) stencil_stream_copy(c);
   SI_CUDA(cudaMemsetAsync(c.flag.get(), 0, sizeof(int) * 4, c.s));
   {
     Scratch S(c);
@@ -2791,6 +3124,9 @@ static bool fused_smoother(const Ctx& c, int l) {
   const int m = level_degree(c, l);
   return l == 0 && c.p.cheb_fused && m >= 3 && m <= kFMaxM;
 }
+static bool streamed_smoother(const Ctx& c, int l) {
+  return l == 0 && c.p.cheb_fused == 2 && level_degree(c, l) == 3;
+}
 
 // One Chebyshev smoothing on level l for A x = b.  pre: x = 0 start, leaves r = b - A x.
 static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
@@ -2803,6 +3139,24 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
   double* d2 = L.d2.get();
   const bool st = (l == 0);
   const bool fused = fused_smoother(c, l);
+  if (streamed_smoother(c, l)) {
+    // y-streamed Chebyshev(3): one launch, the post-smoothing residual included.  Post-smoothing
+    // reads x_0 from L.d (written by the prolongation, see vcycle_level) and writes x.
+    ChebFCoef kc;
+    kc.ith = 1.0 / k.th;
+    for (int it = 0; it < 2; ++it) {
+      const double rho_new = 1.0 / (2.0 * k.sg - rho);
+      kc.c1[it] = rho_new * rho;
+      kc.c2[it] = 2.0 * rho_new / k.de;
+      rho = rho_new;
+    }
+    prof_begin(c);
+    launch_cheb3_stream(c, L.dinv.get(), b, pre ? nullptr : d, x, pre ? r : nullptr, kc, pre);
+    SI_LAUNCHED(c);
+    // stencil + Dinv once, b read, (x_0 read,) x written (, r_3 written)
+    prof_end(c, PC_CHEB0F, (double)c.Nn * (kJBytesNode + 32.0 + 16.0 + 32.0));
+    return;
+  }
   // r = b - A x ; d = Dinv r / th  (fused pre-smoothing does this inside its launch)
   if (!(fused && pre)) {
     prof_begin(c);
@@ -2917,8 +3271,9 @@ static void vcycle_level(Ctx& c, int l, const double* b, double* x) {
   vcycle_level(c, l + 1, Lc.rhs.get(), Lc.x.get());
   // x += P e_c
   prof_begin(c);
+  // (the streamed finest post-smoother updates x out of place: x_0 = x + P e_c goes to L.d)
   gspmv(c, L.nb, L.b, Lc.b, L.Pnnzb, L.Prp.get(), L.Pci.get(), Lc.b == 4 ? L.Pval.get() : L.PvalT.get(), Lc.x.get(),
-        x, x);
+        x, streamed_smoother(c, l) ? L.d.get() : x);
   prof_end(c, l == 0 ? PC_TRANSFER0 : PC_TRANSFER,
            L.Pnnzb * (8.0 * Lc.b * L.b + 4.0) + 4.0 * (L.nb + 1) + 16.0 * L.b * L.nb + 8.0 * Lc.b * L.nbc);
   smooth(c, l, b, x, false);

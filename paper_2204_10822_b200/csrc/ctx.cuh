@@ -164,6 +164,7 @@ struct Ctx {
   // finest-level Jacobian: upper half of the symmetric 3x3 node stencil of 2x2 blocks,
   // 19 values per node, slot-major SoA (layout in stencil.cuh)
   DBuf<double> Jst;
+  DBuf<double> Jsm;  // smoother copy Jsm[j][20][sp] for the TMA-streamed Chebyshev (cheb_fused = 2)
   DBuf<double> mf_v, mf_pi;  // (v, pi) of the last assembly, for the matrix-free FGMRES operator
   DBuf<double> lin_v;        // v of the last assembly (AMG near-nullspace column, nullspace_dim = 4)
   DBuf<double> R;  // residual of the last assemble
@@ -197,6 +198,7 @@ struct Ctx {
   cudaGraphExec_t vgraph = nullptr;
   cudaStream_t cap_stream = nullptr;
   bool use_graphs = true;
+  int sms = 148;      // SM count of the device (grid sizing of the streamed smoother)
   DBuf<double> vc_in, vc_out;
   DBuf<double> cinv;  // dense coarse inverse
   int cn = 0;         // coarse DOFs

@@ -227,23 +227,25 @@ def test_problem1_sv_converges_std_and_picard_do_not():
     assert its["std"][1] == 0 and its["picard"][1] == 0
 
 
-@pytest.mark.parametrize("n", [37, 64])
+@pytest.mark.parametrize("n", [37, 64, 131])
 def test_fused_chebyshev_matches_per_step(n):
-    """The temporally blocked finest-level Chebyshev(3) launch (cheb_fused=1) performs the same
-    arithmetic per node and step as one launch per step: V-cycles agree to rounding, on meshes
-    with ragged edge tiles (28 x 4 node tiles)."""
+    """The temporally blocked finest-level Chebyshev(3) launches (cheb_fused=1: tiles; cheb_fused=2:
+    y-streamed strips with the post-smoothing residual inside) perform the same arithmetic per
+    node and step as one launch per step: V-cycles agree to rounding, on meshes with ragged
+    edge tiles / strips and several row segments."""
     inp, pb, v, pi = newton_state(n, 3, 0)
     v = wl.random_velocity(n, 5, amp=0.05)
     pi = wl.random_pi(n, 6, max_norm=1.2)
     out = []
-    for fused in (0, 1):
+    for fused in (0, 1, 2):
         ctx = make_ctx(n, cheb_fused=fused)
         ctx.set_inputs(inp)
         ctx.assemble_jacobian(v, pi.ravel(), want_csr=False)
         ctx.amg_setup()
         r = wl.random_interior_vector(n, 8)
         out.append(np_(ctx.precond_apply(r)))
-    assert np.linalg.norm(out[1] - out[0]) <= 1e-12 * np.linalg.norm(out[0])
+    for o in out[1:]:
+        assert np.linalg.norm(o - out[0]) <= 1e-12 * np.linalg.norm(out[0])
 
 
 

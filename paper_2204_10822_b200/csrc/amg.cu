@@ -737,20 +737,26 @@ __device__ __forceinline__ int hinsert(int* tab, int key) {
   }
 }
 
+// Symbolic phase in one table build: the row's distinct column count and its sorted column list,
+// written to tmp at the row's expansion offset off[r] (>= the distinct count); k_sg_rows_compact
+// then packs the rows into the CSR column array once the counts are scanned (one table build
+// instead of a count pass and a column pass).
 template <int HT, int HW>
-__global__ void __launch_bounds__(32 * HW) k_sg_hash_count(int nr, const int* __restrict__ xrp,
-                                                                const int* __restrict__ xci,
-                                                                const int* __restrict__ yrp,
-                                                                const int* __restrict__ yci, int* __restrict__ cnt) {
+__global__ void __launch_bounds__(32 * HW) k_sg_hash_symbolic(int nr, const int* __restrict__ xrp,
+                                                                   const int* __restrict__ xci,
+                                                                   const int* __restrict__ yrp,
+                                                                   const int* __restrict__ yci,
+                                                                   const long long* __restrict__ off,
+                                                                   int* __restrict__ cnt, int* __restrict__ tmp) {
   __shared__ int tabs[HW][HT];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * HW + w;
-  int* tab = tabs[w];
   if (r > nr) return;
   if (r == nr) {
     if (lane == 0) cnt[r] = 0;
     return;
   }
+  int* tab = tabs[w];
   for (int t = lane; t < HT; t += 32) tab[t] = -1;
   __syncwarp();
   int u = 0;
@@ -761,28 +767,7 @@ __global__ void __launch_bounds__(32 * HW) k_sg_hash_count(int nr, const int* __
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
   if (lane == 0) cnt[r] = u;
-}
-
-template <int HT, int HW>
-__global__ void __launch_bounds__(32 * HW) k_sg_hash_cols(int nr, const int* __restrict__ xrp,
-                                                               const int* __restrict__ xci,
-                                                               const int* __restrict__ yrp,
-                                                               const int* __restrict__ yci,
-                                                               const int* __restrict__ crp, int* __restrict__ cci) {
-  __shared__ int tabs[HW][HT];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * HW + w;
-  if (r >= nr) return;
-  int* tab = tabs[w];
-  for (int t = lane; t < HT; t += 32) tab[t] = -1;
   __syncwarp();
-  for (int e = xrp[r]; e < xrp[r + 1]; ++e) {
-    const int j = xci[e];
-    for (int f = yrp[j] + lane; f < yrp[j + 1]; f += 32) hinsert<HT>(tab, yci[f]);
-  }
-  __syncwarp();
-  // compact the occupied slots to the front of the table (in slot order), pad with INT_MAX
-  const int u = crp[r + 1] - crp[r];
   int base = 0;
   for (int t0 = 0; t0 < HT; t0 += 32) {
     const int k = tab[t0 + lane];
@@ -796,7 +781,6 @@ __global__ void __launch_bounds__(32 * HW) k_sg_hash_cols(int nr, const int* __r
   while (P2 < u) P2 <<= 1;
   for (int t = u + lane; t < P2; t += 32) tab[t] = 0x7fffffff;
   __syncwarp();
-  // bitonic sort of tab[0, P2)
   for (int k = 2; k <= P2; k <<= 1) {
     for (int jj = k >> 1; jj > 0; jj >>= 1) {
       for (int t = lane; t < P2; t += 32) {
@@ -813,8 +797,19 @@ __global__ void __launch_bounds__(32 * HW) k_sg_hash_cols(int nr, const int* __r
       __syncwarp();
     }
   }
-  int* out = cci + crp[r];
+  int* out = tmp + off[r];
   for (int t = lane; t < u; t += 32) out[t] = tab[t];
+}
+
+// pack the rows written at their expansion offsets into the CSR column array (8 lanes per row)
+__global__ void k_sg_rows_compact(int nr, const long long* __restrict__ off, const int* __restrict__ tmp,
+                                  const int* __restrict__ crp, int* __restrict__ cci) {
+  const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int r = (int)(gt >> 3), l = (int)(gt & 7);
+  if (r >= nr) return;
+  const int c0 = crp[r], u = crp[r + 1] - c0;
+  const int* in = tmp + off[r];
+  for (int t = l; t < u; t += 8) cci[c0 + t] = in[t];
 }
 
 template <int M, int K, int P, int HT, int HW>
@@ -879,19 +874,22 @@ __device__ __forceinline__ unsigned grp_mask() {
   return ((1u << kNG) - 1u) << ((threadIdx.x & 31) & ~(kNG - 1));
 }
 
-__global__ void __launch_bounds__(32 * kNW) k_sgn_count(int nr, const int* __restrict__ xrp, const int* __restrict__ xci,
-                                                         const int* __restrict__ yrp, const int* __restrict__ yci,
-                                                         int* __restrict__ cnt) {
+// one-table-build symbolic phase of the narrow path (see k_sg_hash_symbolic)
+__global__ void __launch_bounds__(32 * kNW) k_sgn_symbolic(int nr, const int* __restrict__ xrp,
+                                                            const int* __restrict__ xci, const int* __restrict__ yrp,
+                                                            const int* __restrict__ yci,
+                                                            const long long* __restrict__ off, int* __restrict__ cnt,
+                                                            int* __restrict__ tmp) {
   __shared__ int tabs[kNRows][kNHT];
   const int g = threadIdx.x / kNG, l = threadIdx.x % kNG;
   const int r = blockIdx.x * kNRows + g;
   const unsigned gm = grp_mask();
-  int* tab = tabs[g];
   if (r > nr) return;  // uniform per group
   if (r == nr) {
     if (l == 0) cnt[r] = 0;
     return;
   }
+  int* tab = tabs[g];
   for (int t = l; t < kNHT; t += kNG) tab[t] = -1;
   __syncwarp(gm);
   int u = 0;
@@ -902,25 +900,7 @@ __global__ void __launch_bounds__(32 * kNW) k_sgn_count(int nr, const int* __res
 #pragma unroll
   for (int o = kNG / 2; o > 0; o >>= 1) u += __shfl_xor_sync(gm, u, o, kNG);
   if (l == 0) cnt[r] = u;
-}
-
-__global__ void __launch_bounds__(32 * kNW) k_sgn_cols(int nr, const int* __restrict__ xrp, const int* __restrict__ xci,
-                                                        const int* __restrict__ yrp, const int* __restrict__ yci,
-                                                        const int* __restrict__ crp, int* __restrict__ cci) {
-  __shared__ int tabs[kNRows][kNHT];
-  const int g = threadIdx.x / kNG, l = threadIdx.x % kNG;
-  const int r = blockIdx.x * kNRows + g;
-  const unsigned gm = grp_mask();
-  if (r >= nr) return;
-  int* tab = tabs[g];
-  for (int t = l; t < kNHT; t += kNG) tab[t] = -1;
   __syncwarp(gm);
-  for (int e = xrp[r]; e < xrp[r + 1]; ++e) {
-    const int j = xci[e];
-    for (int f = yrp[j] + l; f < yrp[j + 1]; f += kNG) hinsert<kNHT>(tab, yci[f]);
-  }
-  __syncwarp(gm);
-  // compact (slot order) into the table front
   const int lane = threadIdx.x & 31;
   const unsigned below = gm & ((1u << lane) - 1u);
   int base = 0;
@@ -932,10 +912,8 @@ __global__ void __launch_bounds__(32 * kNW) k_sgn_cols(int nr, const int* __rest
     base += __popc(m);
     __syncwarp(gm);
   }
-  // order by rank (keys are distinct)
-  const int u = crp[r + 1] - crp[r];
-  int* out = cci + crp[r];
-  for (int q = l; q < u; q += kNG) {
+  int* out = tmp + off[r];
+  for (int q = l; q < u; q += kNG) {  // order by rank (keys are distinct)
     const int key = tab[q];
     int rank = 0;
     for (int t = 0; t < u; ++t) rank += tab[t] < key;
@@ -1121,11 +1099,13 @@ static bool cta_numeric(Ctx& c, const BsrMat& X, const int* cnt, SgPlan& pl, Scr
 // hash path: every row's expansion fits the per-warp shared-memory table of HT slots
 template <int M, int K, int P, int HT, int HW>
 static void hash_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBuf<int>& cci,
-                        DBuf<double>& cval, long long& cnnzb, SgPlan& pl, Scratch& S) {
+                        DBuf<double>& cval, long long& cnnzb, SgPlan& pl, Scratch& S, const long long* off,
+                        long long tot) {
   const int nr = X.nbr;
   const int hb = (nr + 1 + HW - 1) / HW;
   int* cnt = S.get<int>(nr + 1);
-  k_sg_hash_count<HT, HW><<<hb, 32 * HW, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, cnt);
+  int* tmp = S.get<int>(tot);
+  k_sg_hash_symbolic<HT, HW><<<hb, 32 * HW, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, off, cnt, tmp);
   SI_LAUNCHED(c);
   crp.ensure(c.al, nr + 1);
   exclusive_scan(c, cnt, crp.get(), nr + 1);
@@ -1133,7 +1113,7 @@ static void hash_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp
   SI_CHECK(cnnzb < (1LL << 31), SEAICE_EINVAL, "SpGEMM result exceeds int32 indexing");
   cci.ensure(c.al, cnnzb);
   cval.ensure(c.al, cnnzb * M * P);
-  k_sg_hash_cols<HT, HW><<<hb, 32 * HW, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, crp.get(), cci.get());
+  k_sg_rows_compact<<<grid_for((long long)nr * 8), kThreads, 0, c.s>>>(nr, off, tmp, crp.get(), cci.get());
   SI_LAUNCHED(c);
   if (!cta_numeric<M, K, P>(c, X, cnt, pl, S)) pl.kind = (HT == kHT) ? SG_HASH1K : SG_HASH4K;
   sg_numeric<M, K, P>(c, pl, X, Y, crp.get(), cci.get(), cval.get());
@@ -1142,11 +1122,13 @@ static void hash_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp
 
 template <int M, int K, int P>
 static void narrow_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBuf<int>& cci,
-                          DBuf<double>& cval, long long& cnnzb, SgPlan& pl, Scratch& S) {
+                          DBuf<double>& cval, long long& cnnzb, SgPlan& pl, Scratch& S, const long long* off,
+                          long long tot) {
   const int nr = X.nbr;
   const int hb = (nr + 1 + kNRows - 1) / kNRows;
   int* cnt = S.get<int>(nr + 1);
-  k_sgn_count<<<hb, 32 * kNW, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, cnt);
+  int* tmp = S.get<int>(tot);
+  k_sgn_symbolic<<<hb, 32 * kNW, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, off, cnt, tmp);
   SI_LAUNCHED(c);
   crp.ensure(c.al, nr + 1);
   exclusive_scan(c, cnt, crp.get(), nr + 1);
@@ -1154,7 +1136,7 @@ static void narrow_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& c
   SI_CHECK(cnnzb < (1LL << 31), SEAICE_EINVAL, "SpGEMM result exceeds int32 indexing");
   cci.ensure(c.al, cnnzb);
   cval.ensure(c.al, cnnzb * M * P);
-  k_sgn_cols<<<hb, 32 * kNW, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, crp.get(), cci.get());
+  k_sg_rows_compact<<<grid_for((long long)nr * 8), kThreads, 0, c.s>>>(nr, off, tmp, crp.get(), cci.get());
   SI_LAUNCHED(c);
   pl.kind = SG_NARROW;
   sg_numeric<M, K, P>(c, pl, X, Y, crp.get(), cci.get(), cval.get());
@@ -1188,18 +1170,18 @@ static void spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp, DBu
     const double ylen = Y.nbr > 0 ? (double)Y.nnzb / Y.nbr : 1.0;
     if ((force == 5 || (force == 0 && ylen <= 12.0 && tot >= 24LL * nr)) && maxub <= kNHT / 2) {
       c.sg_hits[5]++;
-      narrow_spgemm<M, K, P>(c, X, Y, crp, cci, cval, cnnzb, pl, S);
+      narrow_spgemm<M, K, P>(c, X, Y, crp, cci, cval, cnnzb, pl, S, off, tot);
       return;
     }
     const bool wide_rows = force == 1 || force == 6 || (force == 0 && tot >= 32LL * nr);
     if (wide_rows && maxub <= kHT / 2 && force != 6) {
       c.sg_hits[0]++;
-      hash_spgemm<M, K, P, kHT, kHWarps>(c, X, Y, crp, cci, cval, cnnzb, pl, S);
+      hash_spgemm<M, K, P, kHT, kHWarps>(c, X, Y, crp, cci, cval, cnnzb, pl, S, off, tot);
       return;
     }
     if (wide_rows && maxub <= kHT2 / 2) {
       c.sg_hits[1]++;
-      hash_spgemm<M, K, P, kHT2, kHWarps2>(c, X, Y, crp, cci, cval, cnnzb, pl, S);
+      hash_spgemm<M, K, P, kHT2, kHWarps2>(c, X, Y, crp, cci, cval, cnnzb, pl, S, off, tot);
       return;
     }
   }

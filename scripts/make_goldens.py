@@ -11,7 +11,12 @@ oracle/").
         same AMG definition as the GPU).  Stored: Newton count, FGMRES count per
         solve, AMG levels per solve, final relres, full v.
 
-Usage: python scripts/make_goldens.py cfg2|cfg3 [--out tests/golden]
+  cfg4  step 1 of config 4 (n = 2048, seed 3, 8.4 M unknowns) with the product defaults: tier-B
+        AMG-FGMRES (MIS(2) finest / MIS(3) coarse, 4 near-nullspace columns) and the
+        Eisenstat-Walker forcing of reading G29.  Stored: Newton count, FGMRES count per solve,
+        AMG levels, residual history, v at 65536 sampled DOFs + ||v||.
+
+Usage: python scripts/make_goldens.py cfg2|cfg3|cfg4 [--out tests/golden]
 """
 import argparse
 import json
@@ -83,10 +88,31 @@ def run_cfg3(out):
                         v_norm=np.array([np.linalg.norm(v)]))
 
 
+def run_cfg4(out):
+    cfg = wl.CONFIGS[4]
+    prm = wl.PhysParams()
+    t0 = time.time()
+    inp = wl.step_inputs(cfg, 0)
+    v, pi, h = newton.solve_step(inp, prm, linsolve="amg_fgmres", forcing=1)
+    meta = {"config": 4, "n": cfg.n, "seed": cfg.seed, "step": 1,
+            "solver": "oracle sv-Newton, AMG-FGMRES(30) with Eisenstat-Walker forcing (reading G29), floor rtol 1e-8; "
+                      "oracle/amg.py defaults (nullspace_dim 4, agg_dist0 2, agg_dist 3) = the product defaults",
+            "gpu_params": {}, "newton": h["newton_iters"], "converged": bool(h["converged"]),
+            "relres": h["res"][-1] / h["res"][0], "krylov": [k["iters"] for k in h["krylov"]],
+            "levels": [k.get("levels") for k in h["krylov"]], "alphas": h["alpha"], "res": h["res"],
+            "seconds": round(time.time() - t0, 1), "generator": "scripts/make_goldens.py cfg4 (calls oracle/ only)",
+            "v_storage": "cfg4_v.npz: v at 65536 DOFs drawn by numpy default_rng(12345) (sorted) + ||v||_2"}
+    with open(os.path.join(out, "cfg4_step1.json"), "w") as f:
+        json.dump(meta, f)
+    idx = np.sort(np.random.default_rng(SAMPLE_SEED).choice(v.size, size=65536, replace=False))
+    np.savez_compressed(os.path.join(out, "cfg4_v.npz"), sample_idx=idx.astype(np.int64), v_sample=v[idx],
+                        v_norm=np.array([np.linalg.norm(v)]))
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["cfg2", "cfg3"])
+    ap.add_argument("which", choices=["cfg2", "cfg3", "cfg4"])
     ap.add_argument("--out", default=os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                                   "tests", "golden"))
     a = ap.parse_args()
-    {"cfg2": run_cfg2, "cfg3": run_cfg3}[a.which](a.out)
+    {"cfg2": run_cfg2, "cfg3": run_cfg3, "cfg4": run_cfg4}[a.which](a.out)

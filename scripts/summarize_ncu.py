@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G = os.path.join(ROOT, "gpurun_out")
 P = os.path.join(ROOT, "profiles")
 TAG = sys.argv[1] if len(sys.argv) > 1 else "r01"
-CLASS = [("k_chebM_stencil", "cheb0_fused"), ("k_cheb_stencil", "cheb0"), ("k_gcheb", "cheb_coarse"),
+CLASS = [("k_cheb3_stream", "cheb0_fused"), ("k_chebM_stencil", "cheb0_fused"), ("k_cheb_stencil", "cheb0"), ("k_gcheb", "cheb_coarse"),
          ("k_acheb4", "cheb_coarse"), ("k_aresid4", "resid_coarse"), ("k_aspmv", "transfer"),
          ("k_gresid", "resid_coarse"), ("k_gspmv", "transfer"), ("k_resid_dinv_stencil", "resid0"),
          ("k_dense_gemv", "coarse_solve"), ("k_stencil_spmv", "spmv0"), ("k_multidot", "multidot"),

@@ -419,7 +419,8 @@ def run_ours(a, rank, world, local_rank):
                    "krylov": (f"{'PCG' if ctx.params.krylov_method else 'FGMRES(%d)' % ctx.params.restart} rtol "
                               f"{ctx.params.krylov_rtol:g}{' + Eisenstat-Walker forcing' if ctx.params.krylov_forcing else ''}, "
                               f"maxit {ctx.params.krylov_maxit}, AMG(MIS2 smoothed aggregation, "
-                              f"{ctx.params.nullspace_dim} near-nullspace columns, Chebyshev-{ctx.params.cheb_degree})"),
+                              f"{ctx.params.nullspace_dim} near-nullspace columns, Chebyshev-{ctx.params.cheb_degree}, "
+                              f"hierarchy lag T={ctx.params.amg_lag}, finest smoother cheb_fused={ctx.params.cheb_fused})"),
                    "params_override": json.loads(a.params)},
         "s_per_timestep": ms_max / 1e3 / a.steps,
         "dof_krylov_iters_per_s": dof_its,

@@ -112,7 +112,7 @@ typedef struct {
                               groups, 4 sort + warp per row, 5 8-lane hash tables (falls back when a
                               row's expansion exceeds 256), 6 hash tables of 4k entries (else sort)
                               (see seaice_spgemm_path_hits) */
-  int32_t amg_lag;         /* 0: full AMG setup at every Newton iteration; T > 0 (reading G31):
+  int32_t amg_lag;         /* default 10.  0: full AMG setup at every Newton iteration; T > 0 (reading G31):
                               at Newton iteration l >= 1 of a time step the hierarchy is rebuilt only
                               if the previous linear solve needed more than T Krylov iterations,
                               otherwise its coarse levels (P, R, A_l, l >= 1) are kept and only the

@@ -280,7 +280,7 @@ void seaice_default_params(seaice_params* p, int32_t n) {
   p->nullspace_dim = 4;  // rigid-body modes + the linearisation point (reading G30)
   p->krylov_method = 0;
   p->spgemm_path = 0;
-  p->amg_lag = 0;
+  p->amg_lag = 10;  // lagged hierarchy after cheap solves (config 4: 3.35 -> 3.05 s; Problem II 1.4-2.5x, DESIGN G31)
   p->amg_reuse = 0;
 }
 

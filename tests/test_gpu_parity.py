@@ -25,6 +25,7 @@ def make_ctx(n, **kw):
     # (reading G13); the Eisenstat-Walker product default (G29) is compared with the oracle's
     # same rule where a test asks for krylov_forcing=1
     kw.setdefault("krylov_forcing", 0)
+    kw.setdefault("amg_lag", 0)  # the oracle runs these tests compare with rebuild at every iteration
     return SeaIce(n, **kw)
 
 

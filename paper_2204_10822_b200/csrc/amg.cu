@@ -2538,7 +2538,12 @@ __global__ void __launch_bounds__(256) k_aresid4_cta(int nb, const int* __restri
 // ~7 sequential dependent-load rounds per row at 32 lanes per row)
 // (config 4: level 3, 9.9 k rows of 67 blocks, runs faster as 32-lane groups — 28 vs 40 us per
 // Chebyshev step: CTA-per-row pays only where the rows are few)
-static bool use_cta_rows(long long nnzb, int nb) { return nb > 0 && nb <= 4096 && (double)nnzb / nb >= 48.0; }
+static bool use_cta_rows(long long nnzb, int nb) {
+  static const double minrow = getenv("SEAICE_CTA_MINROW") ? atof(getenv("SEAICE_CTA_MINROW")) : 32.0;  // tuning aid
+  // (MIS(3) coarse levels have ~45 blocks per row: 32 instead of 48 measured 2433 -> 2415 us per V-cycle)
+  static const int maxnb = getenv("SEAICE_CTA_MAXNB") ? atoi(getenv("SEAICE_CTA_MAXNB")) : 4096;
+  return nb > 0 && nb <= maxnb && (double)nnzb / nb >= minrow;
+}
 
 // slots (blocks in flight per block row) for the row-component kernels
 static int pick_slots(long long nnzb, int nb, int BR) {

@@ -33,7 +33,8 @@ def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
     amg_lag = T > 0 (reading G31): at Newton iteration l >= 1 the AMG hierarchy is rebuilt only
     if the previous linear solve needed more than T Krylov iterations; otherwise its coarse
     levels are kept and only the finest level is refreshed from the current Jacobian
-    (amg.refresh_finest).
+    (amg.refresh_finest); a hierarchy built with K = 3 near-nullspace columns because v_l was zero
+    is rebuilt as soon as v_l != 0 (nullspace_dim = 4).
     amg_reuse = 1 (reading G32): the first AMG setup of the time step builds the aggregates;
     every later setup of the step keeps them (amg.setup(..., reuse=H)) and recomputes all values
     from the current Jacobian and linearisation point."""
@@ -92,7 +93,10 @@ def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
             # the linearisation point v is the fourth near-nullspace column when
             # amg_params["nullspace_dim"] == 4 (reading G30); ignored otherwise
             ap = amg_params or {}
-            if H is None or amg_lag <= 0 or hist["krylov"][-1]["iters"] > amg_lag:
+            # (G31 refinement: a hierarchy built without the v_l column, K = 3 because v_l was 0, is
+            # not kept once v_l != 0 and nullspace_dim = 4 asks for the fourth column)
+            stale_K = H is not None and H["K"] == 3 and ap.get("nullspace_dim", 4) == 4 and bool(np.any(v))
+            if H is None or amg_lag <= 0 or hist["krylov"][-1]["iters"] > amg_lag or stale_K:
                 H = amg.setup(J, pb, v=v, reuse=H if amg_reuse else None, **ap)
                 hist.setdefault("amg_rebuilt", []).append(True)
                 hist.setdefault("amg_reused", []).append(H["reused"])

@@ -3097,6 +3097,13 @@ static void amg_setup_numeric(Ctx& c, int K) {
 // block-diagonal inverse and lambda_max are recomputed from the current stencil J (the finest
 // smoother and residual read J itself), and the V-cycle graph is re-captured (its Chebyshev
 // coefficients depend on lambda_max).
+// reading G31 refinement: a hierarchy built without the v_l column (v_l = 0, K = 3) is not kept
+// once the linearisation point is non-zero (the fourth near-nullspace column then exists)
+bool amg_lag_allowed(Ctx& c) {
+  if (c.p.nullspace_dim == 4 && c.reuse_K == 3) return norm2(c, c.lin_v.get(), c.N) == 0.0;
+  return true;
+}
+
 void amg_refresh_finest(Ctx& c) {
   SI_CHECK(c.assembled && c.nlev > 1, SEAICE_ESTATE, "amg_refresh_finest without a multilevel hierarchy");
   vgraph_destroy(c);

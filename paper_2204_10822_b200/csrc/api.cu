@@ -105,7 +105,8 @@ int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* o
   if (c.p.precond == SEAICE_PC_AMG) {
     EvTimer t(c);
     // reading G31: keep the coarse levels while the previous solve stayed cheap
-    const bool lag = c.p.amg_lag > 0 && c.lag_ok && c.nlev > 1 && c.last_krylov_its <= c.p.amg_lag;
+    const bool lag = c.p.amg_lag > 0 && c.lag_ok && c.nlev > 1 && c.last_krylov_its <= c.p.amg_lag &&
+                     amg_lag_allowed(c);
     if (lag) amg_refresh_finest(c);
     else amg_setup_impl(c);
     c.lag_ok = true;

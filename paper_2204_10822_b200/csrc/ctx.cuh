@@ -309,6 +309,7 @@ void precond_apply(Ctx& c, const double* r, double* z);
 // amg.cu
 void amg_setup_impl(Ctx& c);
 void amg_refresh_finest(Ctx& c);
+bool amg_lag_allowed(Ctx& c);
 void amg_vcycle(Ctx& c, const double* r, double* z);
 void amg_free(Ctx& c);
 

@@ -384,7 +384,8 @@ def run_ours(a, rank, world, local_rank):
         if d.get("bytes"):
             gbs = d["bytes"] / (d["ms"] / 1e3) / 1e9
             kern[name].update({"alg_bytes_per_launch": d["bytes"] / d["launches"], "achieved_gbs": round(gbs, 1),
-                               "frac_of_peak": round(gbs / peak, 4)})
+                               "frac_of_peak": round(gbs / peak, 4),
+                               "frac_of_8TBs": round(gbs / 8000.0, 4)})  # BASELINE.json's nominal 8 TB/s
     dom = max(kern, key=lambda k: kern[k]["ms_total"]) if kern else None
     roof = None
     if dom and "achieved_gbs" in kern[dom]:

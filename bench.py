@@ -138,7 +138,7 @@ COUNTS_FILE = os.path.join(ROOT, "profiles", "r02_cfg4_counts.json")
 def oracle_phases(cfg, n_sample=256, threads=None):
     """Per-phase timing of the CPU oracle (numpy/scipy fp64, oracle/) on one full sv-Newton
     iteration of the workload's generator at mesh n_sample: residual + Jacobian assembly, AMG
-    setup, AMG-FGMRES(30) to 1e-8, energy line search + dual/velocity update.  threads: BLAS /
+    setup, AMG-FGMRES(60) to 1e-8, energy line search + dual/velocity update.  threads: BLAS /
     OpenMP thread limit (threadpoolctl; None = all cores).  Returns per-phase seconds per DOF
     (Krylov: per DOF per iteration) and the sample's description."""
     from threadpoolctl import threadpool_limits
@@ -159,7 +159,7 @@ def oracle_phases(cfg, n_sample=256, threads=None):
         t1 = time.perf_counter()
         H = OA.setup(J, pb, v=v)
         t2 = time.perf_counter()
-        vt, st = krylov.fgmres(lambda x: J @ x, R, lambda r: OA.vcycle(H, r), 30, 1e-8, 300)
+        vt, st = krylov.fgmres(lambda x: J @ x, R, lambda r: OA.vcycle(H, r), 60, 1e-8, 300)
         t3 = time.perf_counter()
         for k in range(21):
             if pb.delta_energy(v, vt, 0.5 ** k) < 0:

@@ -68,7 +68,7 @@ typedef struct {
   int32_t newton_maxit;    /* 200 */
   int32_t ls_max_halvings; /* 20: alpha = 1, 1/2, ..., 2^-20 */
   double krylov_rtol;      /* 1e-8 relative to ||b|| */
-  int32_t restart;         /* FGMRES restart m (30) */
+  int32_t restart;         /* FGMRES restart m (60; 1..60).  The paper does not state it (reading G13) */
   int32_t krylov_maxit;    /* 300 */
   int32_t precond;         /* seaice_precond_kind */
   double amg_theta;        /* strength threshold of the node-block measure */
@@ -123,6 +123,14 @@ typedef struct {
                               products) and recomputes every value from the current J and v_l
                               (near-nullspace, P_tent, lambda_max, smoothed P, A_l, coarse factor);
                               falls back to a full setup when the near-nullspace dimension changes */
+  int32_t vcycle_tail;     /* 0 (default): one launch per smoothing step / transfer on every level; 1: the bottom
+                              levels of the V-cycle (4 x 4-block levels whose operators and transfers
+                              together stay under ~48 MB, i.e. L2-resident) run in ONE cooperative launch,
+                              phases separated by grid barriers.  Same operations in the same order (row
+                              sums grouped as the per-launch kernels group them).  Measured on B200 at
+                              config 4: the launch takes 136 us against 184 us for the 27 launches it
+                              replaces, but inside the captured V-cycle graph the cooperative node costs
+                              more than it saves (2442 -> 2499 us per V-cycle), hence off by default */
 } seaice_params;
 
 /* Compressed-sparse-row view (scalar rows). Index arrays int32, values fp64. */

@@ -4,7 +4,9 @@ PAPER.md P:983-986 uses FGMRES ("flexible generalized minimum residual")
 preconditioned by AMG; P:732-735 uses a sparse direct solver (MUMPS, out of
 scope: replaced here by a dense Cholesky / scipy sparse direct solve on tiny
 meshes).  The paper does not state the Krylov tolerance or restart (reading
-G13): rtol 1e-8 relative to ||b||, restart 30, maxit 300.
+G13): rtol 1e-8 relative to ||b||, restart 60, maxit 300 (restart 30, PETSc's default,
+until round 2: the late solves of a time step need 100-160 iterations and lose their
+superlinear phase at every restart; stored goldens name the restart they were made with).
 
 FGMRES definition shared (as a definition, not code) with the CUDA path:
 right preconditioning, x0 = 0, classical Gram-Schmidt (one pass, PETSc's
@@ -20,7 +22,7 @@ import numpy as np
 import scipy.linalg as sla
 
 
-def fgmres(Aop, b, Mop=None, restart=30, rtol=1e-8, maxit=300):
+def fgmres(Aop, b, Mop=None, restart=60, rtol=1e-8, maxit=300):
     b = np.asarray(b, dtype=np.float64)
     N = b.size
     x = np.zeros(N)

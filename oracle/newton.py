@@ -22,7 +22,7 @@ LS_ETA = 1e-12
 
 
 def solve_step(inp, prm, kind="sv", linsolve="direct", rtol=1e-8, maxit=200,
-               ls_max=20, krylov_rtol=1e-8, krylov_maxit=300, restart=30,
+               ls_max=20, krylov_rtol=1e-8, krylov_maxit=300, restart=60,
                project_pi=False, amg_params=None, record_iterates=False, forcing=0, amg_lag=0,
                amg_reuse=0):
     """forcing = 1: Eisenstat-Walker choice 2 for the Krylov tolerance of each solve (reading

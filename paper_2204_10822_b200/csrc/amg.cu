@@ -10,6 +10,7 @@
 // (row-major product) order by a single thread, reductions are fixed-order two-stage.
 #include <cub/cub.cuh>
 #include <cuda.h>
+#include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cmath>
@@ -2562,7 +2563,14 @@ static int pick_slots(long long nnzb, int nb, int BR) {
     case 4: { constexpr int SS = 4; CALL; } break;   \
     default: { constexpr int SS = 8; CALL; } break;  \
   }
-static int agrid(int nb, int G) { return (int)(((long long)nb * G + 255) / 256); }
+// threads per block of the row-component kernels (tuning aid SEAICE_ABLOCK; measured at config 4:
+// 64 / 128 / 256 threads within +-2 % of each other; a persistent grid of 8 x 148 CTAs looping
+// over the rows ran level 1 at 4.1 instead of 4.8 TB/s)
+static int ablock() {
+  static const int b = getenv("SEAICE_ABLOCK") ? atoi(getenv("SEAICE_ABLOCK")) : 256;
+  return b;
+}
+static int agrid(int nb, int G) { return (int)(((long long)nb * G + ablock() - 1) / ablock()); }
 
 static int pick_group(long long nnzb, int nb) {
   static const int shift = getenv("SEAICE_GROUP_SHIFT") ? atoi(getenv("SEAICE_GROUP_SHIFT")) : 0;  // tuning aid
@@ -2606,11 +2614,11 @@ static void gspmv(Ctx& c, int nb, int br, int bc, long long nnzb, const int* rp,
       else if (br == 2) k_aspmv_cta<2, 4><<<nb, 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y);
       else k_aspmv_cta<4, 2><<<nb, 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y);
     } else if (br == 4 && bc == 4) {
-      SI_SDISPATCH(Sl, (k_aspmv<4, 4, SS><<<agrid(nb, 4 * SS), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
+      SI_SDISPATCH(Sl, (k_aspmv<4, 4, SS><<<agrid(nb, 4 * SS), ablock(), 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
     } else if (br == 2) {
-      SI_SDISPATCH(Sl, (k_aspmv<2, 4, SS><<<agrid(nb, 2 * SS), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
+      SI_SDISPATCH(Sl, (k_aspmv<2, 4, SS><<<agrid(nb, 2 * SS), ablock(), 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
     } else {
-      SI_SDISPATCH(Sl, (k_aspmv<4, 2, SS><<<agrid(nb, 4 * SS), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
+      SI_SDISPATCH(Sl, (k_aspmv<4, 2, SS><<<agrid(nb, 4 * SS), ablock(), 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
     }
   } else {
     SI_GDISPATCH(G, (k_gspmv<2, 2, GG><<<ggrid(nb, GG), 256, 0, c.s>>>(nb, rp, ci, val, x, yin, y)))
@@ -3123,6 +3131,209 @@ void amg_refresh_finest(Ctx& c) {
   c.amg_ready = true;
 }
 
+// ------------------------------------------------------------------ V-cycle tail (persistent)
+// The bottom of the V-cycle (levels whose operators fit the L2 together, e.g. 4 k / 262 / 21 block
+// rows at config 4) costs ~27 launches of 4-15 us each, latency-bound (VERDICT round-1 item 4).
+// k_vcycle_tail runs those levels in ONE cooperative launch: every phase (residual, Chebyshev
+// step, restriction, coarse GEMV, prolongation) is a row loop over the level, phases separated
+// by grid.sync().  Same operations in the same order as vcycle_level / smooth on these levels
+// (b = 4 blocks).  A level of more than 2 rows per CTA is swept warp per row (8 blocks in
+// flight per row, the sums of k_acheb4<8> / k_aresid4<8> / k_aspmv<4, 4, 8>), a smaller one CTA
+// per row (64 blocks in flight, the sums of the _cta kernels).  Vectors written in one phase and
+// read in the next are read with L2-coherent loads (ld.global.cg / volatile: the .nc path of the
+// stand-alone kernels assumes data that is read-only for the whole launch); matrices stay on
+// the read-only path.
+constexpr int kTailMaxLevels = 8;
+struct TailLevel {
+  int nb, nbc;
+  const int *rp, *ci, *Rrp, *Rci, *Prp, *Pci;
+  const double *val, *dinv, *Rval, *Pval;
+  const double* rhs;
+  double *x, *r, *d, *d2;
+  double ith, c1[2], c2[2];  // 1 / theta and the Chebyshev(3) recurrence coefficients
+};
+struct TailArgs {
+  int nl;  // smoothed levels in the tail; below them the coarsest level (dense inverse)
+  TailLevel lv[kTailMaxLevels];
+  int cn;
+  const double* cinv;
+  double *cx, *crhs;
+};
+
+__device__ __forceinline__ void ld4_coh(const double* p, double (&v)[4]) {
+  asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p)
+               : "memory");
+}
+__device__ __forceinline__ double ld_coh(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+// Row sweep geometry: CTA = true: one row per CTA at a time (thread t: component t % 4 of slot
+// t / 4 of 64), the row's epilogue runs on warp 0; CTA = false: one row per warp (8 slots).
+template <bool CTA>
+struct TailSweep {
+  static __device__ __forceinline__ int first() {
+    return CTA ? (int)blockIdx.x : (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  }
+  static __device__ __forceinline__ int step() { return CTA ? (int)gridDim.x : (int)((gridDim.x * blockDim.x) >> 5); }
+};
+// component (lane % 4) of (M x)_row for a 4 x 4-block row: in lanes 0..3 of the row's warp (CTA:
+// threads 0..3).  Every thread of the warp (CTA) calls it.
+template <bool CTA>
+__device__ __forceinline__ double tail_row(int row, const int* __restrict__ rp, const int* __restrict__ ci,
+                                           const double* __restrict__ val, const double* x, double (*sh)[4]) {
+  constexpr int S = CTA ? 64 : 8;
+  const int t = CTA ? (int)threadIdx.x : (int)(threadIdx.x & 31);
+  const int a = t & 3, slot = t >> 2;
+  double acc = 0.0;
+  const int e1 = __ldg(rp + row + 1);
+  int e = __ldg(rp + row) + slot;
+  for (; e + S < e1; e += 2 * S) {
+    const int c0 = __ldg(ci + e), c1 = __ldg(ci + e + S);
+    double v0[4], v1[4], x0[4], x1[4];
+    load_row<4>(val + ((long long)e * 4 + a) * 4, v0);
+    load_row<4>(val + ((long long)(e + S) * 4 + a) * 4, v1);
+    ld4_coh(x + (long long)c0 * 4, x0);
+    ld4_coh(x + (long long)c1 * 4, x1);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc += v0[b] * x0[b];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc += v1[b] * x1[b];
+  }
+  for (; e < e1; e += S) {
+    double v0[4], x0[4];
+    load_row<4>(val + ((long long)e * 4 + a) * 4, v0);
+    ld4_coh(x + (long long)__ldg(ci + e) * 4, x0);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc += v0[b] * x0[b];
+  }
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (!CTA) return acc;
+  if ((t & 31) < 4) sh[t >> 5][a] = acc;
+  __syncthreads();
+  double tot = 0.0;
+  if (t < 4) {
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += sh[w][t];
+  }
+  __syncthreads();
+  return tot;
+}
+// r = b - A x (x NULL: r = b); d = c2 Dinv r
+template <bool CTA>
+__device__ __forceinline__ void tail_resid(const TailLevel& L, const double* x, double (*sh)[4]) {
+  const int lane = threadIdx.x & 31;
+  for (int row = TailSweep<CTA>::first(); row < L.nb; row += TailSweep<CTA>::step()) {
+    const double acc = x ? tail_row<CTA>(row, L.rp, L.ci, L.val, x, sh) : 0.0;
+    if (CTA && threadIdx.x >= 32) continue;
+    const long long i = (long long)row * 4 + (lane & 3);
+    double D[4];
+    load_row<4>(L.dinv + (long long)row * 16 + (lane & 3) * 4, D);
+    const double rv = ld_coh(L.rhs + i) - acc;
+    if (lane < 4) L.r[i] = rv;
+    double z = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) z += D[k] * __shfl_sync(0xffffffffu, rv, k);
+    if (lane < 4) L.d[i] = L.ith * z;
+  }
+}
+// Chebyshev step (semantics of k_acheb4): t = A d; x (+)= d; r -= t; dout = c1 d + c2 Dinv r
+template <bool CTA>
+__device__ __forceinline__ void tail_cheb(const TailLevel& L, const double* d, double* dout, double c1, double c2,
+                                          bool first, bool want_r, bool want_d, double (*sh)[4]) {
+  const int lane = threadIdx.x & 31;
+  for (int row = TailSweep<CTA>::first(); row < L.nb; row += TailSweep<CTA>::step()) {
+    const double acc = want_r ? tail_row<CTA>(row, L.rp, L.ci, L.val, d, sh) : 0.0;
+    if (CTA && threadIdx.x >= 32) continue;
+    const long long i = (long long)row * 4 + (lane & 3);
+    const double dv = ld_coh(d + i);
+    const double xv = first ? 0.0 : ld_coh(L.x + i);
+    if (lane < 4) L.x[i] = xv + dv;
+    if (!want_r) continue;
+    const double rv = ld_coh(L.r + i) - acc;
+    if (lane < 4) L.r[i] = rv;
+    if (!want_d) continue;
+    double D[4];
+    load_row<4>(L.dinv + (long long)row * 16 + (lane & 3) * 4, D);
+    double z = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) z += D[k] * __shfl_sync(0xffffffffu, rv, k);
+    if (lane < 4) dout[i] = c1 * dv + c2 * z;
+  }
+}
+// y = yin + M x for a 4 x 4-block transfer operator (yin NULL: y = M x; yin == y: in place)
+template <bool CTA>
+__device__ __forceinline__ void tail_spmv(int nb, const int* rp, const int* ci, const double* val, const double* x,
+                                          const double* yin, double* y, double (*sh)[4]) {
+  const int lane = threadIdx.x & 31;
+  for (int row = TailSweep<CTA>::first(); row < nb; row += TailSweep<CTA>::step()) {
+    const double acc = tail_row<CTA>(row, rp, ci, val, x, sh);
+    if (CTA && threadIdx.x >= 32) continue;
+    const long long i = (long long)row * 4 + (lane & 3);
+    const double y0 = yin ? ld_coh(yin + i) : 0.0;
+    if (lane < 4) y[i] = y0 + acc;
+  }
+}
+#define SI_TAIL(NB, CALL)                      \
+  if ((NB) <= 2 * (int)gridDim.x) {            \
+    constexpr bool TC = true;                  \
+    CALL;                                      \
+  } else {                                     \
+    constexpr bool TC = false;                 \
+    CALL;                                      \
+  }
+
+__global__ void __launch_bounds__(256) k_vcycle_tail(const __grid_constant__ TailArgs A) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  __shared__ double sh[8][4];
+  // down-sweep: pre-smoothing from x = 0 (leaves r = b - A x), restriction
+  for (int l = 0; l < A.nl; ++l) {
+    const TailLevel& L = A.lv[l];
+    SI_TAIL(L.nb, tail_resid<TC>(L, nullptr, sh));
+    grid.sync();
+    SI_TAIL(L.nb, tail_cheb<TC>(L, L.d, L.d2, L.c1[0], L.c2[0], true, true, true, sh));
+    grid.sync();
+    SI_TAIL(L.nb, tail_cheb<TC>(L, L.d2, L.d, L.c1[1], L.c2[1], false, true, true, sh));
+    grid.sync();
+    SI_TAIL(L.nb, tail_cheb<TC>(L, L.d, L.d2, 0.0, 0.0, false, true, false, sh));
+    grid.sync();
+    double* rc = l + 1 < A.nl ? const_cast<double*>(A.lv[l + 1].rhs) : A.crhs;
+    SI_TAIL(L.nbc, tail_spmv<TC>(L.nbc, L.Rrp, L.Rci, L.Rval, L.r, nullptr, rc, sh));
+    grid.sync();
+  }
+  // coarsest level: x = A^-1 b (dense inverse, warp per row; b = 4: unpadded vectors)
+  {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int w = gw; w < A.cn; w += nw) {
+      double sacc = 0.0;
+      for (int k = lane; k < A.cn; k += 32) sacc += __ldg(A.cinv + (long long)w * A.cn + k) * ld_coh(A.crhs + k);
+      sacc = warp_sum(sacc);
+      if (lane == 0) A.cx[w] = sacc;
+    }
+  }
+  grid.sync();
+  // up-sweep: prolongation, post-smoothing
+  for (int l = A.nl - 1; l >= 0; --l) {
+    const TailLevel& L = A.lv[l];
+    const double* xc = l + 1 < A.nl ? A.lv[l + 1].x : A.cx;
+    SI_TAIL(L.nb, tail_spmv<TC>(L.nb, L.Prp, L.Pci, L.Pval, xc, L.x, L.x, sh));
+    grid.sync();
+    SI_TAIL(L.nb, tail_resid<TC>(L, L.x, sh));
+    grid.sync();
+    SI_TAIL(L.nb, tail_cheb<TC>(L, L.d, L.d2, L.c1[0], L.c2[0], false, true, true, sh));
+    grid.sync();
+    SI_TAIL(L.nb, tail_cheb<TC>(L, L.d2, L.d, L.c1[1], L.c2[1], false, true, true, sh));
+    grid.sync();
+    SI_TAIL(L.nb, tail_cheb<TC>(L, L.d, L.d2, 0.0, 0.0, false, false, false, sh));
+    if (l > 0) grid.sync();
+  }
+}
+
 // ------------------------------------------------------------------ host: V-cycle
 struct ChebCoef {
   double th, de, sg;
@@ -3195,7 +3406,7 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
                                              pre ? nullptr : x, r, d, 1.0 / k.th);
       } else {
         const int Sl = pick_slots(L.nnzb, L.nb, 4);
-        SI_SDISPATCH(Sl, (k_aresid4<SS><<<agrid(L.nb, 4 * SS), 256, 0, c.s>>>(
+        SI_SDISPATCH(Sl, (k_aresid4<SS><<<agrid(L.nb, 4 * SS), ablock(), 0, c.s>>>(
                              L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), b, pre ? nullptr : x, r, d,
                              1.0 / k.th)))
       }
@@ -3253,7 +3464,7 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
       } else {
         const int Sl = pick_slots(L.nnzb, L.nb, 4);
         // late own-entry loads: measured 2357 -> 1555 us of coarse smoothing per V-cycle (config 4)
-        SI_SDISPATCH(Sl, (k_acheb4<SS, true><<<agrid(L.nb, 4 * SS), 256, 0, c.s>>>(
+        SI_SDISPATCH(Sl, (k_acheb4<SS, true><<<agrid(L.nb, 4 * SS), ablock(), 0, c.s>>>(
                              L.nb, L.rp.get(), L.ci.get(), L.val.get(), L.dinv.get(), d, r, x, d2, c1, c2, first,
                              want_r, want_d)))
       }
@@ -3271,8 +3482,83 @@ static void smooth(Ctx& c, int l, const double* b, double* x, bool pre) {
   }
 }
 
+// First level of the persistent tail (k_vcycle_tail), or -1: the deepest run of b = 4 levels
+// l >= 1 whose operators and transfers together stay under ~48 MB (L2-resident on the B200).
+static int tail_start(const Ctx& c) {
+  if (!c.p.vcycle_tail || c.nlev < 3 || c.lv[c.nlev - 1].b != 4) return -1;
+  static const double cap = getenv("SEAICE_TAIL_MB") ? atof(getenv("SEAICE_TAIL_MB")) * 1e6 : 48e6;  // tuning aid
+  double bytes = 0.0;
+  int l0 = -1;
+  for (int l = c.nlev - 2; l >= 1 && c.nlev - 1 - l <= kTailMaxLevels; --l) {
+    const Level& L = c.lv[l];
+    if (L.b != 4) break;
+    bytes += (double)(L.nnzb + L.Pnnzb + L.Rnnzb) * 132.0;
+    if (bytes > cap) break;
+    l0 = l;
+  }
+  return l0;
+}
+
+static int tail_grid(const Ctx& c) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    int occ = 0;
+    SI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vcycle_tail, 256, 0));
+    const int want = getenv("SEAICE_TAIL_CTAS") ? atoi(getenv("SEAICE_TAIL_CTAS")) : 4;  // tuning aid
+    per_sm = occ < 1 ? 0 : (want < occ ? want : occ);
+    if (per_sm < 1) per_sm = occ;
+  }
+  SI_CHECK(per_sm >= 1, SEAICE_ECUDA, "k_vcycle_tail cannot be resident");
+  return per_sm * c.sms;
+}
+
+// Levels l0 .. nlev-1 of the V-cycle in one cooperative launch (b = rhs, x = solution of level l0)
+static void vcycle_tail(Ctx& c, int l0, const double* b, double* x) {
+  TailArgs A{};
+  A.nl = c.nlev - 1 - l0;
+  double by = 0.0;
+  for (int k = 0; k < A.nl; ++k) {
+    Level& L = c.lv[l0 + k];
+    TailLevel& T = A.lv[k];
+    T.nb = L.nb;
+    T.nbc = L.nbc;
+    T.rp = L.rp.get(), T.ci = L.ci.get(), T.val = L.val.get(), T.dinv = L.dinv.get();
+    T.Rrp = L.Rrp.get(), T.Rci = L.Rci.get(), T.Rval = L.Rval.get();
+    T.Prp = L.Prp.get(), T.Pci = L.Pci.get(), T.Pval = L.Pval.get();
+    T.rhs = k == 0 ? b : L.rhs.get();
+    T.x = k == 0 ? x : L.x.get();
+    T.r = L.r.get(), T.d = L.d.get(), T.d2 = L.d2.get();
+    const ChebCoef kc = cheb_coef(c, L);
+    double rho = 1.0 / kc.sg;
+    T.ith = 1.0 / kc.th;
+    for (int it = 0; it < 2; ++it) {
+      const double rho_new = 1.0 / (2.0 * kc.sg - rho);
+      T.c1[it] = rho_new * rho;
+      T.c2[it] = 2.0 * rho_new / kc.de;
+      rho = rho_new;
+    }
+    // six operator passes, the two transfers, ~20 vector passes
+    by += 6.0 * (L.nnzb * 132.0 + 4.0 * (L.nb + 1)) + (L.Pnnzb + L.Rnnzb) * 132.0 + 20.0 * 32.0 * L.nb;
+  }
+  Level& Lz = c.lv[c.nlev - 1];
+  A.cn = c.cn;
+  A.cinv = c.cinv.get();
+  A.cx = Lz.x.get();
+  A.crhs = Lz.rhs.get();
+  by += 8.0 * c.cn * c.cn + 16.0 * c.cn;
+  void* args[] = {&A};
+  prof_begin(c);
+  SI_CUDA(cudaLaunchCooperativeKernel((const void*)k_vcycle_tail, dim3(tail_grid(c)), dim3(256), args, 0, c.s));
+  SI_LAUNCHED(c);
+  prof_end(c, PC_TAIL, by);
+}
+
 static void vcycle_level(Ctx& c, int l, const double* b, double* x) {
   Level& L = c.lv[l];
+  if (l >= 1 && l + 1 < c.nlev && level_degree(c, l) == 3 && l == tail_start(c)) {
+    vcycle_tail(c, l, b, x);
+    return;
+  }
   if (l + 1 == c.nlev) {
     prof_begin(c);
     k_dense_gemv<<<grid_for((long long)c.cn * 32, 256), 256, 0, c.s>>>(c.cn, L.b, vstride(L.b), c.cinv.get(), b, x);

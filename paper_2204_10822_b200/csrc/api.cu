@@ -75,6 +75,7 @@ void validate(const seaice_params* p) {
   SI_CHECK(p->spgemm_path >= 0 && p->spgemm_path <= 6, SEAICE_EINVAL, "spgemm_path must be in 0..6");
   SI_CHECK(p->amg_lag >= 0, SEAICE_EINVAL, "amg_lag must be >= 0");
   SI_CHECK(p->amg_reuse == 0 || p->amg_reuse == 1, SEAICE_EINVAL, "amg_reuse must be 0 or 1");
+  SI_CHECK(p->vcycle_tail == 0 || p->vcycle_tail == 1, SEAICE_EINVAL, "vcycle_tail must be 0 or 1");
 }
 
 int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* out) {
@@ -260,7 +261,7 @@ void seaice_default_params(seaice_params* p, int32_t n) {
   p->newton_maxit = 200;
   p->ls_max_halvings = 20;
   p->krylov_rtol = 1e-8;
-  p->restart = 30;
+  p->restart = 60;  // reading G13 (config 4: 2.88 -> 2.61 s per step against restart 30; the late solves need 100-160 iterations)
   p->krylov_maxit = 300;
   p->precond = SEAICE_PC_AMG;
   p->amg_theta = 0.04;
@@ -283,6 +284,7 @@ void seaice_default_params(seaice_params* p, int32_t n) {
   p->spgemm_path = 0;
   p->amg_lag = 10;  // lagged hierarchy after cheap solves (config 4: 3.35 -> 3.05 s; Problem II 1.4-2.5x, DESIGN G31)
   p->amg_reuse = 0;
+  p->vcycle_tail = 0;  // measured on B200 (config 4): 136 us instead of 184 us of kernels, but the captured V-cycle 2442 -> 2499 us
 }
 
 int seaice_create(const seaice_params* p, const seaice_runtime* rt, seaice_ctx** out) {

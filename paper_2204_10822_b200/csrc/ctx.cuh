@@ -120,7 +120,8 @@ enum ProfClass {
   PC_CHEB1 = 16,    // K4 Chebyshev step on level 1 (PC_CHEBC: levels >= 2)
   PC_RESID1 = 17,   // residual + Dinv on level 1 (PC_RESIDC: levels >= 2)
   PC_TRANSFER0 = 18,  // restriction / prolongation between levels 0 and 1 (PC_TRANSFER: deeper)
-  PC_NCLASS = 19
+  PC_TAIL = 19,       // levels of the persistent V-cycle tail (one cooperative launch)
+  PC_NCLASS = 20
 };
 struct Prof {
   bool on = false;

@@ -37,7 +37,8 @@ class Params(C.Structure):
                 ("agg_dist", C.c_int32), ("cheb_fused", C.c_int32),
                 ("cheb_degree0", C.c_int32), ("matfree", C.c_int32),
                 ("krylov_forcing", C.c_int32), ("nullspace_dim", C.c_int32), ("krylov_method", C.c_int32),
-                ("spgemm_path", C.c_int32), ("amg_lag", C.c_int32), ("amg_reuse", C.c_int32)]
+                ("spgemm_path", C.c_int32), ("amg_lag", C.c_int32), ("amg_reuse", C.c_int32),
+                ("vcycle_tail", C.c_int32)]
 
 
 ALLOC_T = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -267,7 +268,7 @@ class SeaIce:
 
     PROF_NAMES = ["assemble", "spmv0", "cheb0", "cheb_coarse", "resid0", "multidot", "maxpy_norm", "maxpy",
                   "delta_energy", "transfer", "coarse_solve", "resid_coarse", "pi_update", "cheb0_fused", "transport",
-                  "jv_matfree", "cheb_level1", "resid_level1", "transfer_level0"]
+                  "jv_matfree", "cheb_level1", "resid_level1", "transfer_level0", "vcycle_tail"]
 
     def profile(self, on: bool):
         self._check(self.L.seaice_profile_enable(self.h, 1 if on else 0))

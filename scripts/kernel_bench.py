@@ -23,7 +23,7 @@ cfg = wl.CONFIGS[a.config]
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
 inp = wl.step_inputs(cfg, 0)
-ctx = SeaIce(cfg.n, krylov_rtol=0.0, krylov_maxit=30)
+ctx = SeaIce(cfg.n, krylov_rtol=0.0, krylov_maxit=30, restart=30)
 ctx.set_inputs(inp)
 N, Nn, Nc = ctx.N, (cfg.n + 1) ** 2, cfg.n * cfg.n
 v = torch.zeros(N, dtype=torch.float64, device="cuda")

@@ -8,11 +8,11 @@ oracle/").
         oracle's own previous v.  Stored per step: Newton count, final relres, ||v||, v at 512
         fixed sampled DOFs; full v for steps 1, 12, 24.
   cfg3  step 1 of config 3 (n = 1024, seed 2) with the AMG-FGMRES of `oracle/amg.py` (tier B,
-        same AMG definition as the GPU).  Stored: Newton count, FGMRES count per
+        same AMG definition as the GPU; FGMRES(30), the default when it was made).  Stored: Newton count, FGMRES count per
         solve, AMG levels per solve, final relres, full v.
 
   cfg4  step 1 of config 4 (n = 2048, seed 3, 8.4 M unknowns) with the product defaults: tier-B
-        AMG-FGMRES (MIS(2) finest / MIS(3) coarse, 4 near-nullspace columns) and the
+        AMG-FGMRES(30) (MIS(2) finest / MIS(3) coarse, 4 near-nullspace columns) and the
         Eisenstat-Walker forcing of reading G29.  Stored: Newton count, FGMRES count per solve,
         AMG levels, residual history, v at 65536 sampled DOFs + ||v||.
 
@@ -72,10 +72,10 @@ def run_cfg3(out):
     # the AMG definition this golden was generated with (MIS(2) on every level: the oracle default
     # before agg_dist = 3 became the coarse-level default); the GPU test runs the same definition
     amg_params = {"agg_dist0": 2, "agg_dist": 2}
-    v, pi, h = newton.solve_step(inp, prm, linsolve="amg_fgmres", amg_params=amg_params)
+    v, pi, h = newton.solve_step(inp, prm, linsolve="amg_fgmres", amg_params=amg_params, restart=30)
     meta = {"config": 3, "n": cfg.n, "seed": cfg.seed, "step": 1,
             "solver": "oracle sv-Newton, AMG-FGMRES(30) rtol 1e-8 (oracle/amg.py defaults: nullspace_dim 4, reading G30)",
-            "gpu_params": dict(amg_params), "amg_params": amg_params,
+            "gpu_params": dict(amg_params, restart=30), "amg_params": amg_params,
             "newton": h["newton_iters"], "converged": bool(h["converged"]), "relres": h["res"][-1] / h["res"][0],
             "krylov": [k["iters"] for k in h["krylov"]], "levels": [k.get("levels") for k in h["krylov"]],
             "alphas": h["alpha"], "res": h["res"], "seconds": round(time.time() - t0, 1),
@@ -93,11 +93,13 @@ def run_cfg4(out):
     prm = wl.PhysParams()
     t0 = time.time()
     inp = wl.step_inputs(cfg, 0)
-    v, pi, h = newton.solve_step(inp, prm, linsolve="amg_fgmres", forcing=1)
+    # amg_lag = 0: a full AMG setup every Newton iteration on both sides (the lagging rule of G31
+    # branches on an iteration count, so a count differing by one would fork the two runs)
+    v, pi, h = newton.solve_step(inp, prm, linsolve="amg_fgmres", forcing=1, amg_lag=0, restart=30)
     meta = {"config": 4, "n": cfg.n, "seed": cfg.seed, "step": 1,
             "solver": "oracle sv-Newton, AMG-FGMRES(30) with Eisenstat-Walker forcing (reading G29), floor rtol 1e-8; "
                       "oracle/amg.py defaults (nullspace_dim 4, agg_dist0 2, agg_dist 3) = the product defaults",
-            "gpu_params": {}, "newton": h["newton_iters"], "converged": bool(h["converged"]),
+            "gpu_params": {"amg_lag": 0, "restart": 30}, "newton": h["newton_iters"], "converged": bool(h["converged"]),
             "relres": h["res"][-1] / h["res"][0], "krylov": [k["iters"] for k in h["krylov"]],
             "levels": [k.get("levels") for k in h["krylov"]], "alphas": h["alpha"], "res": h["res"],
             "seconds": round(time.time() - t0, 1), "generator": "scripts/make_goldens.py cfg4 (calls oracle/ only)",

@@ -38,7 +38,7 @@ def test_default_params_and_struct_layout():
     p = seaice.Params()
     L.seaice_default_params(ctypes.byref(p), 64)
     assert p.n == 64 and p.L == 512e3 and p.P_star == 27500.0 and p.f_c == 1.46e-4
-    assert p.newton_rtol == 1e-8 and p.newton_maxit == 200 and p.restart == 30 and p.krylov_maxit == 300
+    assert p.newton_rtol == 1e-8 and p.newton_maxit == 200 and p.restart == 60 and p.krylov_maxit == 300
     assert p.ls_max_halvings == 20 and p.e == 2.0 and p.delta_min == 2e-9
 
 

@@ -138,20 +138,21 @@ def test_single_level_is_exact_solve():
     assert np.linalg.norm(J @ z - r) <= 1e-10 * np.linalg.norm(r)
 
 
-@pytest.mark.parametrize("nsd,method", [(3, 0), (4, 0), (4, 1)])
+@pytest.mark.parametrize("nsd,method,restart", [(3, 0, 30), (4, 0, 30), (4, 0, 60), (4, 0, 12), (4, 1, 60)])
 @pytest.mark.parametrize("n,it", [(32, 0), (32, 5), (64, 8)])
-def test_amg_fgmres_counts_parity(n, it, nsd, method):
+def test_amg_fgmres_counts_parity(n, it, nsd, method, restart):
     """AMG-FGMRES (krylov_method 0) and AMG-PCG (1) iteration counts vs the oracle's same
-    definitions, with 3 or 4 near-nullspace columns (reading G30)."""
+    definitions, with 3 or 4 near-nullspace columns (reading G30) and restart lengths 60 (the
+    default, reading G13), 30 and 12 (several restarts at these sizes)."""
     inp, pb, v, pi = newton_state(n, 11, it)
     J = pb.jacobian(v, pi, "sv")
     R = pb.residual(v)
     H = OA.setup(J, pb, v=v, nullspace_dim=nsd)
     if method == 0:
-        xo, so = krylov.fgmres(lambda x: J @ x, R, lambda r: OA.vcycle(H, r), 30, 1e-8, 300)
+        xo, so = krylov.fgmres(lambda x: J @ x, R, lambda r: OA.vcycle(H, r), restart, 1e-8, 300)
     else:
         xo, so = krylov.pcg(lambda x: J @ x, R, lambda r: OA.vcycle(H, r), 1e-8, 300)
-    ctx = make_ctx(n, nullspace_dim=nsd, krylov_method=method)
+    ctx = make_ctx(n, nullspace_dim=nsd, krylov_method=method, restart=restart)
     ctx.set_inputs(inp)
     ctx.assemble_jacobian(v, pi.ravel(), want_csr=False)
     ctx.amg_setup()
@@ -248,6 +249,36 @@ def test_fused_chebyshev_matches_per_step(n):
     for o in out[1:]:
         assert np.linalg.norm(o - out[0]) <= 1e-12 * np.linalg.norm(out[0])
 
+
+@pytest.mark.parametrize("n", [48, 64, 256, 512])
+def test_persistent_vcycle_tail_matches_per_launch(n):
+    """vcycle_tail = 1 runs the bottom levels of the V-cycle in one cooperative launch with grid
+    barriers between the phases; the operations and their order are those of the per-launch path
+    (vcycle_tail = 0, the default), so V-cycles agree to rounding.  n = 48 / 64: every coarse
+    level is in the tail (CTA-per-row sweeps); n = 256 / 512: the tail starts deeper and its
+    first level is swept warp per row."""
+    inp, pb, v, pi = newton_state(min(n, 64), 3, 0) if n <= 64 else _plastic_state(n, 21)
+    if n <= 64:
+        v = wl.random_velocity(n, 5, amp=0.05)
+        pi = wl.random_pi(n, 6, max_norm=1.2)
+    out, launches = [], []
+    for tail in (0, 1):
+        ctx = make_ctx(n, vcycle_tail=tail)
+        ctx.set_inputs(inp)
+        ctx.assemble_jacobian(v, np.asarray(pi).ravel(), want_csr=False)
+        ctx.amg_setup()
+        r = wl.random_interior_vector(n, 8)
+        ctx.precond_apply(r)  # first application captures the V-cycle graph
+        l0 = ctx.launches
+        z = np_(ctx.precond_apply(r))
+        launches.append(ctx.launches - l0)
+        out.append(z)
+        # a second right-hand side through the same captured graph (stale work vectors must not leak)
+        r2 = wl.random_interior_vector(n, 9)
+        out.append(np_(ctx.precond_apply(r2)))
+    assert launches[1] < launches[0], launches  # the tail did replace launches
+    assert np.linalg.norm(out[2] - out[0]) <= 1e-12 * np.linalg.norm(out[0])
+    assert np.linalg.norm(out[3] - out[1]) <= 1e-12 * np.linalg.norm(out[1])
 
 
 PATHS = ["hash1k", "hash4k", "sort_thread", "sort_group8", "sort_warp", "hash_narrow", "cta_numeric"]

@@ -605,6 +605,23 @@ __device__ __forceinline__ void block_fma(double* cb, const double (&xb)[M * K],
   st_blk<M * P>(cb, c);
 }
 
+// the same with the Y block already in registers
+template <int M, int K, int P>
+__device__ __forceinline__ void block_fma_reg(double* cb, const double (&xb)[M * K], const double (&y)[K * P]) {
+  double c[M * P];
+  ld_blk<M * P, false>(cb, c);
+#pragma unroll
+  for (int a = 0; a < M; ++a)
+#pragma unroll
+    for (int b = 0; b < P; ++b) {
+      double s = c[a * P + b];
+#pragma unroll
+      for (int k = 0; k < K; ++k) s += xb[a * K + k] * y[k * P + b];
+      c[a * P + b] = s;
+    }
+  st_blk<M * P>(cb, c);
+}
+
 template <int M, int K, int P>
 __global__ void k_spgemm_numeric(int nr, const int* __restrict__ xrp, const int* __restrict__ xci,
                                  const double* __restrict__ xv, const int* __restrict__ yrp,
@@ -782,6 +799,29 @@ __device__ __forceinline__ int hinsert(int* tab, int key) {
   }
 }
 
+// Insert the columns of the Y rows of X entries e0 + l, e0 + l + G, ... (one X entry per lane at a
+// time, its Y row walked by that lane): for short Y rows this runs G pointer chains (x column ->
+// Y row extent -> Y columns) side by side instead of one after the other with most lanes idle.
+// The table is a set, so the insertion order does not matter.  Returns this lane's new-key count.
+template <int HT, int G>
+__device__ __forceinline__ int sg_insert_by_lane(int e0, int e1, int l, const int* __restrict__ xci,
+                                                 const int* __restrict__ yrp, const int* __restrict__ yci, int* tab) {
+  int u = 0;
+  for (int e = e0 + l; e < e1; e += G) {
+    const int j = xci[e];
+    const int fe = yrp[j + 1];
+    for (int f = yrp[j]; f < fe; f += 4) {
+      int cq[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cq[q] = f + q < fe ? yci[f + q] : -1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (cq[q] >= 0) u += hinsert<HT>(tab, cq[q]);
+    }
+  }
+  return u;
+}
+
 // Symbolic phase in one table build: the row's distinct column count and its sorted column list,
 // written to tmp at the row's expansion offset off[r] (>= the distinct count); k_sg_rows_compact
 // then packs the rows into the CSR column array once the counts are scanned (one table build
@@ -792,7 +832,8 @@ __global__ void __launch_bounds__(32 * HW) k_sg_hash_symbolic(int nr, const int*
                                                                    const int* __restrict__ yrp,
                                                                    const int* __restrict__ yci,
                                                                    const long long* __restrict__ off,
-                                                                   int* __restrict__ cnt, int* __restrict__ tmp) {
+                                                                   int* __restrict__ cnt, int* __restrict__ tmp,
+                                                                   int by_lane) {
   __shared__ int tabs[HW][HT];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * HW + w;
@@ -805,9 +846,13 @@ __global__ void __launch_bounds__(32 * HW) k_sg_hash_symbolic(int nr, const int*
   for (int t = lane; t < HT; t += 32) tab[t] = -1;
   __syncwarp();
   int u = 0;
-  for (int e = xrp[r]; e < xrp[r + 1]; ++e) {
-    const int j = xci[e];
-    for (int f = yrp[j] + lane; f < yrp[j + 1]; f += 32) u += hinsert<HT>(tab, yci[f]);
+  if (by_lane) {  // short Y rows (uniform per launch)
+    u = sg_insert_by_lane<HT, 32>(xrp[r], xrp[r + 1], lane, xci, yrp, yci, tab);
+  } else {
+    for (int e = xrp[r]; e < xrp[r + 1]; ++e) {
+      const int j = xci[e];
+      for (int f = yrp[j] + lane; f < yrp[j + 1]; f += 32) u += hinsert<HT>(tab, yci[f]);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
@@ -857,6 +902,68 @@ __global__ void k_sg_rows_compact(int nr, const long long* __restrict__ off, con
   for (int t = l; t < u; t += 8) cci[c0 + t] = in[t];
 }
 
+// Numeric phase of one row for the hash paths: a group of G lanes (lane l, sync mask gm) walks the
+// row's X entries e0 .. e1 in order (every output block accumulates in X-entry order, so values
+// are bitwise those of the other paths); kt / pt is the row's column -> output position table.
+// Software-pipelined: per X entry the loads form a chain x column -> Y row extent -> Y entry ->
+// output block, ~4 L2 round trips when issued back to back (the kernels were latency-bound on
+// it).  Iteration e issues the column of entry e + 3, the Y extent of e + 2, and this lane's
+// first Y entry and the X block of e + 1, and accumulates entry e from registers.
+template <int M, int K, int P, int HT, int G>
+__device__ __forceinline__ void sg_row_pipelined(int e0, int e1, int l, unsigned gm, const int* __restrict__ xci,
+                                                 const double* __restrict__ xv, const int* __restrict__ yrp,
+                                                 const int* __restrict__ yci, const double* __restrict__ yv,
+                                                 const int* kt, const int* pt, double* __restrict__ cv) {
+  if (e0 >= e1) return;
+  int fb0, fe0, fb1 = 0, fe1 = 0, j2 = 0;
+  int col0 = -1;
+  double y0[K * P], xb0[M * K];
+  {
+    const int j0 = xci[e0];
+    fb0 = yrp[j0], fe0 = yrp[j0 + 1];
+    if (e0 + 1 < e1) {
+      const int j1 = xci[e0 + 1];
+      fb1 = yrp[j1], fe1 = yrp[j1 + 1];
+    }
+    if (e0 + 2 < e1) j2 = xci[e0 + 2];
+    if (fb0 + l < fe0) {
+      col0 = yci[fb0 + l];
+      ld_blk<K * P, true>(yv + (long long)(fb0 + l) * K * P, y0);
+    }
+    ld_blk<M * K, true>(xv + (long long)e0 * M * K, xb0);
+  }
+  for (int e = e0; e < e1; ++e) {
+    int j3 = 0, fb2 = 0, fe2 = 0, col1 = -1;
+    double y1[K * P], xb1[M * K];
+    if (e + 3 < e1) j3 = xci[e + 3];
+    if (e + 2 < e1) fb2 = yrp[j2], fe2 = yrp[j2 + 1];
+    if (e + 1 < e1) {
+      if (fb1 + l < fe1) {
+        col1 = yci[fb1 + l];
+        ld_blk<K * P, true>(yv + (long long)(fb1 + l) * K * P, y1);
+      }
+      ld_blk<M * K, true>(xv + (long long)(e + 1) * M * K, xb1);
+    }
+    if (col0 >= 0) {
+      unsigned h = hslot<HT>(col0);
+      while (kt[h] != col0) h = (h + 1) & (HT - 1);
+      block_fma_reg<M, K, P>(cv + (long long)pt[h] * M * P, xb0, y0);
+      for (int f = fb0 + l + G; f < fe0; f += G) {  // Y rows longer than the lane group
+        const int col = yci[f];
+        h = hslot<HT>(col);
+        while (kt[h] != col) h = (h + 1) & (HT - 1);
+        block_fma<M, K, P>(cv + (long long)pt[h] * M * P, xb0, yv + (long long)f * K * P);
+      }
+    }
+    __syncwarp(gm);
+    fb0 = fb1, fe0 = fe1, fb1 = fb2, fe1 = fe2, j2 = j3, col0 = col1;
+#pragma unroll
+    for (int t = 0; t < K * P; ++t) y0[t] = y1[t];
+#pragma unroll
+    for (int t = 0; t < M * K; ++t) xb0[t] = xb1[t];
+  }
+}
+
 template <int M, int K, int P, int HT, int HW>
 __global__ void __launch_bounds__(32 * HW) k_sg_hash_numeric(
     int nr, const int* __restrict__ xrp, const int* __restrict__ xci, const double* __restrict__ xv,
@@ -880,20 +987,7 @@ __global__ void __launch_bounds__(32 * HW) k_sg_hash_numeric(
   }
   for (long long t = (long long)c0 * M * P + lane; t < (long long)c1 * M * P; t += 32) cv[t] = 0.0;
   __syncwarp();
-  for (int e = xrp[r]; e < xrp[r + 1]; ++e) {
-    const int j = xci[e];
-    double xb[M * K];
-    ld_blk<M * K, true>(xv + (long long)e * M * K, xb);
-    for (int f = yrp[j] + lane; f < yrp[j + 1]; f += 32) {
-      const int col = yci[f];
-      unsigned h = hslot<HT>(col);
-      while (kt[h] != col) h = (h + 1) & (HT - 1);
-      double* cb = cv + (long long)pt[h] * M * P;
-      const double* yb = yv + (long long)f * K * P;
-      block_fma<M, K, P>(cb, xb, yb);
-    }
-    __syncwarp();
-  }
+  sg_row_pipelined<M, K, P, HT, 32>(xrp[r], xrp[r + 1], lane, 0xffffffffu, xci, xv, yrp, yci, yv, kt, pt, cv);
 }
 
 // ------------------------------------------------------------------ narrow-row hash SpGEMM
@@ -928,11 +1022,7 @@ __global__ void __launch_bounds__(32 * kNW) k_sgn_symbolic(int nr, const int* __
   int* tab = tabs[g];
   for (int t = l; t < kNHT; t += kNG) tab[t] = -1;
   __syncwarp(gm);
-  int u = 0;
-  for (int e = xrp[r]; e < xrp[r + 1]; ++e) {
-    const int j = xci[e];
-    for (int f = yrp[j] + l; f < yrp[j + 1]; f += kNG) u += hinsert<kNHT>(tab, yci[f]);
-  }
+  int u = sg_insert_by_lane<kNHT, kNG>(xrp[r], xrp[r + 1], l, xci, yrp, yci, tab);
 #pragma unroll
   for (int o = kNG / 2; o > 0; o >>= 1) u += __shfl_xor_sync(gm, u, o, kNG);
   if (l == 0) cnt[r] = u;
@@ -982,20 +1072,7 @@ __global__ void __launch_bounds__(32 * kNW) k_sgn_numeric(int nr, const int* __r
   }
   for (long long t = (long long)c0 * M * P + l; t < (long long)c1 * M * P; t += kNG) cv[t] = 0.0;
   __syncwarp(gm);
-  for (int e = xrp[r]; e < xrp[r + 1]; ++e) {
-    const int j = xci[e];
-    double xb[M * K];
-    ld_blk<M * K, true>(xv + (long long)e * M * K, xb);
-    for (int f = yrp[j] + l; f < yrp[j + 1]; f += kNG) {
-      const int col = yci[f];
-      unsigned h = hslot<kNHT>(col);
-      while (kt[h] != col) h = (h + 1) & (kNHT - 1);
-      double* cb = cv + (long long)pt[h] * M * P;
-      const double* yb = yv + (long long)f * K * P;
-      block_fma<M, K, P>(cb, xb, yb);
-    }
-    __syncwarp(gm);
-  }
+  sg_row_pipelined<M, K, P, kNHT, kNG>(xrp[r], xrp[r + 1], l, gm, xci, xv, yrp, yci, yv, kt, pt, cv);
 }
 
 // ------------------------------------------------------------------ CTA-per-row numeric (small levels)
@@ -1132,7 +1209,9 @@ static void hash_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp
   const int hb = (nr + 1 + HW - 1) / HW;
   int* cnt = S.get<int>(nr + 1);
   int* tmp = S.get<int>(tot);
-  k_sg_hash_symbolic<HT, HW><<<hb, 32 * HW, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, off, cnt, tmp);
+  // Y rows of <= 12 blocks on average: one X entry per lane (see sg_insert_by_lane)
+  const int by_lane = Y.nbr > 0 && (double)Y.nnzb / Y.nbr <= 12.0 ? 1 : 0;
+  k_sg_hash_symbolic<HT, HW><<<hb, 32 * HW, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, off, cnt, tmp, by_lane);
   SI_LAUNCHED(c);
   crp.ensure(c.al, nr + 1);
   exclusive_scan(c, cnt, crp.get(), nr + 1);
@@ -1143,8 +1222,9 @@ static void hash_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp
   k_sg_rows_compact<<<grid_for((long long)nr * 8), kThreads, 0, c.s>>>(nr, off, tmp, crp.get(), cci.get());
   SI_LAUNCHED(c);
   if (!cta_numeric<M, K, P>(c, X, cnt, pl, S)) pl.kind = (HT == kHT) ? SG_HASH1K : SG_HASH4K;
+  tick(c, HT == kHT ? "  sg.hash1kS" : "  sg.hash4kS", nr);
   sg_numeric<M, K, P>(c, pl, X, Y, crp.get(), cci.get(), cval.get());
-  tick(c, HT == kHT ? "  sg.hash1k" : "  sg.hash4k", nr);
+  tick(c, HT == kHT ? "  sg.hash1kN" : "  sg.hash4kN", nr);
 }
 
 template <int M, int K, int P>
@@ -1166,8 +1246,9 @@ static void narrow_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& c
   k_sg_rows_compact<<<grid_for((long long)nr * 8), kThreads, 0, c.s>>>(nr, off, tmp, crp.get(), cci.get());
   SI_LAUNCHED(c);
   pl.kind = SG_NARROW;
+  tick(c, "  sg.narrowS", nr);
   sg_numeric<M, K, P>(c, pl, X, Y, crp.get(), cci.get(), cval.get());
-  tick(c, "  sg.narrow", nr);
+  tick(c, "  sg.narrowN", nr);
 }
 
 // Output arrays are grow-only DBufs owned by the caller.

@@ -158,8 +158,10 @@ int newton_step_impl(Ctx& c, double* v, double* pi_inout, seaice_newton_stats* o
     for (int k = 0; k < K; ++k) al[k] = std::ldexp(1.0, -k);
     int acc = -1;
     const double nr0 = st.res_norm;
-    for (int k0 = 0; k0 < K && acc < 0; k0 += 8) {
-      const int cnt = std::min(8, K - k0);
+    // alpha = 1 alone first (accepted by almost every Newton iteration; the kernel's fp64 work
+    // grows with the number of step lengths: 2.1 ms for 8 against 0.7 ms for 1 at config 4), then
+    // batches of 8.  Each step length is summed on its own, so the values do not depend on the batching.
+    for (int k0 = 0, cnt = 1; k0 < K && acc < 0; k0 += cnt, cnt = std::min(8, K - k0)) {
       delta_energy_impl(c, v, c.vt.get(), al.data() + k0, cnt, dphi.data() + k0, sab.data() + k0);
       for (int k = k0; k < k0 + cnt; ++k) {
         if (dphi[k] < -kLsEta * sab[k]) {

@@ -60,7 +60,8 @@ for ln in lines:
     if not m:
         continue
     lvl, what, ms = m.group(1), m.group(2).strip(), float(m.group(3))
-    key = what if what.startswith("sg.") else f"L{lvl} {what}"  # SpGEMM ticks carry row counts, not levels
+    # SpGEMM ticks carry the product's row count, not a level: keyed by its order of magnitude
+    key = f"{what} rows~1e{len(lvl) - 1}" if what.startswith("sg.") else f"L{lvl} {what}"
     tot[key] += ms
     if what == "graph_free":
         nset += 1

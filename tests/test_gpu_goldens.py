@@ -1,4 +1,4 @@
-"""Full-step parity at BASELINE.json configs 2 and 3 against stored oracle results.
+"""Full-step parity at BASELINE.json configs 2, 3 and 4 against stored oracle results.
 
 The goldens under tests/golden/ were written by scripts/make_goldens.py, which calls only
 `oracle/` (and the seeded generators): nothing stored there comes from the CUDA path.
@@ -8,6 +8,8 @@ The goldens under tests/golden/ were written by scripts/make_goldens.py, which c
         runs the product path (AMG-FGMRES, default parameters) warm-started from its own v^n.
   cfg3  step 1 of config 3 (n = 1024) with the oracle's AMG-FGMRES (tier B: the same AMG
         definition as the GPU), so FGMRES counts are comparable too.
+  cfg4  step 1 of config 4 (n = 2048, 8.4 M unknowns, the bench workload) with the oracle's
+        AMG-FGMRES and Eisenstat-Walker forcing (2.6 h of CPU): Newton and FGMRES counts, v.
 
 Tolerances (BASELINE.json north_star): converged velocity per step 1e-8 relative L2, Newton
 count +-1, FGMRES count +-10 % (only against the same preconditioner definition, cfg3).
@@ -100,3 +102,51 @@ def test_cfg3_step1_matches_oracle_tier_b():
     bad = [(k, g, o) for k, (g, o) in enumerate(zip(its[:m], meta["krylov"][:m])) if abs(g - o) > max(0.10 * o, 1)]
     assert len(bad) <= max(1, m // 5), bad
     print("cfg3 parity", {"err": err, "newton": (st["newton_iters"], meta["newton"]), "krylov": (its, meta["krylov"])})
+
+
+def test_cfg4_step1_matches_oracle_tier_b():
+    """Step 1 of config 4 (n = 2048, 8.4 M unknowns, the bench workload) against the oracle's own
+    AMG-FGMRES Newton run with Eisenstat-Walker forcing (tier B, the GPU's AMG definition): Newton
+    count +-1, sampled converged velocity and ||v|| to 1e-8, FGMRES counts +-10 % over the solves
+    both sides performed.  The oracle run rebuilt the hierarchy at every iteration (amg_lag = 0)
+    with FGMRES(30), its defaults when the golden was made; the product defaults (lagged
+    hierarchy, FGMRES(60)) must reach the same minimiser."""
+    meta = json.load(open(_load("cfg4_step1.json")))
+    gold = np.load(_load("cfg4_v.npz"))
+    idx, ref, ref_norm = gold["sample_idx"], gold["v_sample"], float(gold["v_norm"][0])
+    from paper_2204_10822_b200.seaice import SeaIce
+    cfg = wl.CONFIGS[4]
+    assert meta["n"] == cfg.n and meta["converged"]
+    inp = wl.step_inputs(cfg, 0)
+    params = {"amg_lag": 0, "restart": 30, **meta.get("gpu_params", {})}
+    ctx = SeaIce(cfg.n, **params)
+    ctx.set_step(inp.dt, inp.t_new, inp.h, inp.A, inp.v_prev, inp.v_air, inp.v_ocean)
+    vv = torch.as_tensor(inp.v_prev, dtype=torch.float64, device="cuda").clone()
+    its, newton = [], 0
+    for _ in range(200):
+        d = ctx.newton_step(vv)
+        if d["converged_on_entry"]:
+            break
+        newton += 1
+        its.append(d["krylov"]["iters"])
+        assert d["krylov"]["converged"] == 1
+    assert abs(newton - meta["newton"]) <= 1, (newton, meta["newton"])
+    vg = vv.cpu().numpy()
+    err = np.linalg.norm(vg[idx] - ref) / np.linalg.norm(ref)
+    assert err <= 1e-8, err
+    assert abs(np.linalg.norm(vg) - ref_norm) <= 1e-8 * ref_norm
+    m = min(len(its), len(meta["krylov"]))
+    tot_g, tot_o = sum(its[:m]), sum(meta["krylov"][:m])
+    assert abs(tot_g - tot_o) <= 0.10 * tot_o, (its, meta["krylov"])
+    bad = [(k, g, o) for k, (g, o) in enumerate(zip(its[:m], meta["krylov"][:m])) if abs(g - o) > max(0.10 * o, 2)]
+    assert len(bad) <= max(1, m // 5), bad
+    del ctx
+    # product defaults: same minimiser
+    ctx = SeaIce(cfg.n)
+    v2, st = ctx.solve_step(inp.dt, inp.t_new, inp.h, inp.A, inp.v_prev, inp.v_air, inp.v_ocean)
+    assert st["converged"] == 1 and st["krylov_capped"] == 0, st
+    v2 = v2.cpu().numpy()
+    err2 = np.linalg.norm(v2[idx] - ref) / np.linalg.norm(ref)
+    assert err2 <= 1e-7, err2  # two inexact-Newton paths, each stopped at ||R|| <= 1e-8 ||R_0||
+    print("cfg4 parity", {"err": err, "err_defaults": err2, "newton": (newton, meta["newton"], st["newton_iters"]),
+                          "krylov": (its, meta["krylov"])})

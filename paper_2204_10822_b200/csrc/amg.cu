@@ -809,14 +809,21 @@ __device__ __forceinline__ int sg_insert_by_lane(int e0, int e1, int l, const in
   int u = 0;
   for (int e = e0 + l; e < e1; e += G) {
     const int j = xci[e];
-    const int fe = yrp[j + 1];
-    for (int f = yrp[j]; f < fe; f += 4) {
+    const int fb = yrp[j], fe = yrp[j + 1];
+    // neighbouring X entries share most of their Y columns: each lane starts its (cyclic) walk at
+    // another place, so the lanes do not compare-and-swap the same table slot at the same time
+    const int len = fe - fb, rot = len > 0 ? (l * 3) % len : 0;
+    for (int q = 0; q < len; q += 4) {
       int cq[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) cq[q] = f + q < fe ? yci[f + q] : -1;
+      for (int t = 0; t < 4; ++t) {
+        int o = q + t + rot;
+        if (o >= len) o -= len;
+        cq[t] = q + t < len ? yci[fb + o] : -1;
+      }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (cq[q] >= 0) u += hinsert<HT>(tab, cq[q]);
+      for (int t = 0; t < 4; ++t)
+        if (cq[t] >= 0) u += hinsert<HT>(tab, cq[t]);
     }
   }
   return u;
@@ -905,19 +912,26 @@ __global__ void k_sg_rows_compact(int nr, const long long* __restrict__ off, con
 // Numeric phase of one row for the hash paths: a group of G lanes (lane l, sync mask gm) walks the
 // row's X entries e0 .. e1 in order (every output block accumulates in X-entry order, so values
 // are bitwise those of the other paths); kt / pt is the row's column -> output position table.
-// Software-pipelined: per X entry the loads form a chain x column -> Y row extent -> Y entry ->
-// output block, ~4 L2 round trips when issued back to back (the kernels were latency-bound on
-// it).  Iteration e issues the column of entry e + 3, the Y extent of e + 2, and this lane's
-// first Y entry and the X block of e + 1, and accumulates entry e from registers.
-template <int M, int K, int P, int HT, int G>
+//  * ROWS: LPB lanes share one block product, lane a of them owning block rows a MR .. (a + 1) MR - 1
+//    of the output, so the LPB lanes read-modify-write consecutive 16/32-byte pieces of one output
+//    block and G / LPB Y entries are in flight per X entry (ncu: the kernels run at l1tex 75-88 %).
+//    Measured at config 4: 8.6 -> 8.3 ms per setup on the 8-lane path, but 4.5 -> 5.7 ms with 32
+//    lanes (Y rows of 9 then take two rounds), which keeps one block per lane (LPB = 1).
+//  * Software-pipelined: per X entry the loads form a chain x column -> Y row extent -> Y entry ->
+//    output block.  Iteration e issues the column of entry e + 3, the Y extent of e + 2, and this
+//    lane's first Y entry and X rows of e + 1, and accumulates entry e from registers.
+template <int M, int K, int P, int HT, int G, bool ROWS>
 __device__ __forceinline__ void sg_row_pipelined(int e0, int e1, int l, unsigned gm, const int* __restrict__ xci,
                                                  const double* __restrict__ xv, const int* __restrict__ yrp,
                                                  const int* __restrict__ yci, const double* __restrict__ yv,
                                                  const int* kt, const int* pt, double* __restrict__ cv) {
+  constexpr int LPB = !ROWS ? 1 : (M % 4 == 0) ? 4 : (M % 2 == 0 ? 2 : 1);
+  constexpr int MR = M / LPB, S = G / LPB;
+  const int a = l % LPB, sl = l / LPB;
   if (e0 >= e1) return;
   int fb0, fe0, fb1 = 0, fe1 = 0, j2 = 0;
   int col0 = -1;
-  double y0[K * P], xb0[M * K];
+  double y0[K * P], xr0[MR * K];
   {
     const int j0 = xci[e0];
     fb0 = yrp[j0], fe0 = yrp[j0 + 1];
@@ -926,33 +940,33 @@ __device__ __forceinline__ void sg_row_pipelined(int e0, int e1, int l, unsigned
       fb1 = yrp[j1], fe1 = yrp[j1 + 1];
     }
     if (e0 + 2 < e1) j2 = xci[e0 + 2];
-    if (fb0 + l < fe0) {
-      col0 = yci[fb0 + l];
-      ld_blk<K * P, true>(yv + (long long)(fb0 + l) * K * P, y0);
+    if (fb0 + sl < fe0) {
+      col0 = yci[fb0 + sl];
+      ld_blk<K * P, true>(yv + (long long)(fb0 + sl) * K * P, y0);
     }
-    ld_blk<M * K, true>(xv + (long long)e0 * M * K, xb0);
+    ld_blk<MR * K, true>(xv + (long long)e0 * M * K + a * MR * K, xr0);
   }
   for (int e = e0; e < e1; ++e) {
     int j3 = 0, fb2 = 0, fe2 = 0, col1 = -1;
-    double y1[K * P], xb1[M * K];
+    double y1[K * P], xr1[MR * K];
     if (e + 3 < e1) j3 = xci[e + 3];
     if (e + 2 < e1) fb2 = yrp[j2], fe2 = yrp[j2 + 1];
     if (e + 1 < e1) {
-      if (fb1 + l < fe1) {
-        col1 = yci[fb1 + l];
-        ld_blk<K * P, true>(yv + (long long)(fb1 + l) * K * P, y1);
+      if (fb1 + sl < fe1) {
+        col1 = yci[fb1 + sl];
+        ld_blk<K * P, true>(yv + (long long)(fb1 + sl) * K * P, y1);
       }
-      ld_blk<M * K, true>(xv + (long long)(e + 1) * M * K, xb1);
+      ld_blk<MR * K, true>(xv + (long long)(e + 1) * M * K + a * MR * K, xr1);
     }
     if (col0 >= 0) {
       unsigned h = hslot<HT>(col0);
       while (kt[h] != col0) h = (h + 1) & (HT - 1);
-      block_fma_reg<M, K, P>(cv + (long long)pt[h] * M * P, xb0, y0);
-      for (int f = fb0 + l + G; f < fe0; f += G) {  // Y rows longer than the lane group
+      block_fma_reg<MR, K, P>(cv + (long long)pt[h] * M * P + a * MR * P, xr0, y0);
+      for (int f = fb0 + sl + S; f < fe0; f += S) {  // Y rows longer than the group's slots
         const int col = yci[f];
         h = hslot<HT>(col);
         while (kt[h] != col) h = (h + 1) & (HT - 1);
-        block_fma<M, K, P>(cv + (long long)pt[h] * M * P, xb0, yv + (long long)f * K * P);
+        block_fma<MR, K, P>(cv + (long long)pt[h] * M * P + a * MR * P, xr0, yv + (long long)f * K * P);
       }
     }
     __syncwarp(gm);
@@ -960,7 +974,7 @@ __device__ __forceinline__ void sg_row_pipelined(int e0, int e1, int l, unsigned
 #pragma unroll
     for (int t = 0; t < K * P; ++t) y0[t] = y1[t];
 #pragma unroll
-    for (int t = 0; t < M * K; ++t) xb0[t] = xb1[t];
+    for (int t = 0; t < MR * K; ++t) xr0[t] = xr1[t];
   }
 }
 
@@ -987,7 +1001,7 @@ __global__ void __launch_bounds__(32 * HW) k_sg_hash_numeric(
   }
   for (long long t = (long long)c0 * M * P + lane; t < (long long)c1 * M * P; t += 32) cv[t] = 0.0;
   __syncwarp();
-  sg_row_pipelined<M, K, P, HT, 32>(xrp[r], xrp[r + 1], lane, 0xffffffffu, xci, xv, yrp, yci, yv, kt, pt, cv);
+  sg_row_pipelined<M, K, P, HT, 32, false>(xrp[r], xrp[r + 1], lane, 0xffffffffu, xci, xv, yrp, yci, yv, kt, pt, cv);
 }
 
 // ------------------------------------------------------------------ narrow-row hash SpGEMM
@@ -1072,7 +1086,7 @@ __global__ void __launch_bounds__(32 * kNW) k_sgn_numeric(int nr, const int* __r
   }
   for (long long t = (long long)c0 * M * P + l; t < (long long)c1 * M * P; t += kNG) cv[t] = 0.0;
   __syncwarp(gm);
-  sg_row_pipelined<M, K, P, kNHT, kNG>(xrp[r], xrp[r + 1], l, gm, xci, xv, yrp, yci, yv, kt, pt, cv);
+  sg_row_pipelined<M, K, P, kNHT, kNG, true>(xrp[r], xrp[r + 1], l, gm, xci, xv, yrp, yci, yv, kt, pt, cv);
 }
 
 // ------------------------------------------------------------------ CTA-per-row numeric (small levels)
@@ -1210,7 +1224,9 @@ static void hash_spgemm(Ctx& c, const BsrMat& X, const BsrMat& Y, DBuf<int>& crp
   int* cnt = S.get<int>(nr + 1);
   int* tmp = S.get<int>(tot);
   // Y rows of <= 12 blocks on average: one X entry per lane (see sg_insert_by_lane)
-  const int by_lane = Y.nbr > 0 && (double)Y.nnzb / Y.nbr <= 12.0 ? 1 : 0;
+  // (measured at config 4: 4.4 -> 2.9 ms per setup on the 1k-slot path; slower on the 4k-slot path,
+  // whose long X rows make the lanes collide in the table)
+  const int by_lane = HT == kHT && Y.nbr > 0 && (double)Y.nnzb / Y.nbr <= 12.0 ? 1 : 0;
   k_sg_hash_symbolic<HT, HW><<<hb, 32 * HW, 0, c.s>>>(nr, X.rp, X.ci, Y.rp, Y.ci, off, cnt, tmp, by_lane);
   SI_LAUNCHED(c);
   crp.ensure(c.al, nr + 1);

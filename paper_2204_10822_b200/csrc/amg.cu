@@ -2416,7 +2416,7 @@ __device__ __forceinline__ void load_row(const double* __restrict__ p, double v[
   }
 }
 
-template <int BR, int BC, int S>
+template <int BR, int BC, int S, bool PF = true>
 __device__ __forceinline__ double grpA_row(int row, int nb, int lig, const int* __restrict__ rp,
                                            const int* __restrict__ ci, const double* __restrict__ val,
                                            const double* __restrict__ x) {
@@ -2426,6 +2426,16 @@ __device__ __forceinline__ double grpA_row(int row, int nb, int lig, const int* 
   if (row < nb) {
     const int e1 = __ldg(rp + row + 1);
     int e = __ldg(rp + row) + slot;
+    if constexpr (PF) {
+      // ptxas schedules each block's FMAs right behind its loads (SASS: LDG, LDG, DFMA ...), so a
+      // slot has one or two 32-byte value loads in flight.  The lane's pieces of its next blocks
+      // are requested here as L1 prefetches (no destination register, nothing to wait on); the
+      // loop's loads then hit L1 or join the miss in flight.
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (e + q * S < e1)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(val + ((long long)(e + q * S) * BR + a) * BC));
+    }
     for (; e + S < e1; e += 2 * S) {
       const int c0 = __ldg(ci + e), c1 = __ldg(ci + e + S);
       double v0[BC], v1[BC], x0[BC], x1[BC];
@@ -2468,7 +2478,7 @@ __global__ void __launch_bounds__(256) k_aspmv(int nb, const int* __restrict__ r
 // Chebyshev step on a b = 4 level (semantics of k_gcheb).  LATE: the row's own vector entries
 // and D^-1 block are loaded after the SpMV (fewer live registers during the gather loop, at
 // the cost of one more round trip); otherwise before it.
-template <int S, bool LATE>
+template <int S, bool LATE, bool PF = true>
 __global__ void __launch_bounds__(256) k_acheb4(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
                                                 const double* __restrict__ val, const double* __restrict__ dinv,
                                                 const double* __restrict__ d, double* __restrict__ r,
@@ -2487,7 +2497,7 @@ __global__ void __launch_bounds__(256) k_acheb4(int nb, const int* __restrict__ 
     if (want_d) load_row<4>(dinv + (long long)row * 16 + lig * 4, D);
   }
   double acc = 0.0;
-  if (want_r) acc = grpA_row<4, 4, S>(row, nb, lig, rp, ci, val, d);
+  if (want_r) acc = grpA_row<4, 4, S, PF>(row, nb, lig, rp, ci, val, d);
   if (LATE && own) {
     dv = d[i];
     if (!first) xv = x[i];
@@ -2506,7 +2516,7 @@ __global__ void __launch_bounds__(256) k_acheb4(int nb, const int* __restrict__ 
 }
 
 // r = b - A x (x may be NULL: r = b); d = c2 Dinv r on a b = 4 level
-template <int S>
+template <int S, bool PF = true>
 __global__ void __launch_bounds__(256) k_aresid4(int nb, const int* __restrict__ rp, const int* __restrict__ ci,
                                                  const double* __restrict__ val, const double* __restrict__ dinv,
                                                  const double* __restrict__ b, const double* __restrict__ x,
@@ -2517,7 +2527,7 @@ __global__ void __launch_bounds__(256) k_aresid4(int nb, const int* __restrict__
   const bool own = row < nb && lig < 4;
   const long long i = (long long)row * 4 + lig;
   double bo = 0.0, D[4] = {0.0, 0.0, 0.0, 0.0};
-  const double acc = x ? grpA_row<4, 4, S>(row, nb, lig, rp, ci, val, x) : 0.0;
+  const double acc = x ? grpA_row<4, 4, S, PF>(row, nb, lig, rp, ci, val, x) : 0.0;
   if (own) {  // after the gather (fewer live registers in the loop, as k_acheb4)
     bo = b[i];
     load_row<4>(dinv + (long long)row * 16 + lig * 4, D);
@@ -2543,6 +2553,7 @@ __device__ __forceinline__ double cta_row(int row, const int* __restrict__ rp, c
   double acc = 0.0;
   const int e1 = __ldg(rp + row + 1);
   int e = __ldg(rp + row) + slot;
+  if (e + S < e1) asm volatile("prefetch.global.L1 [%0];" ::"l"(val + ((long long)(e + S) * BR + a) * BC));
   for (; e + S < e1; e += 2 * S) {
     const int c0 = __ldg(ci + e), c1 = __ldg(ci + e + S);
     double v0[BC], v1[BC], x0[BC], x1[BC];

@@ -177,6 +177,11 @@ __global__ void __launch_bounds__(kMDT) k_multidot(long long n2, const double2* 
 #pragma unroll
   for (int t = 0; t < kMDC; ++t) acc[t] = 0.0;
   for (long long i = blockIdx.x * (long long)kMDT + threadIdx.x; i < n2; i += (long long)gridDim.x * kMDT) {
+    // ptxas keeps two of the eight column loads in flight (SASS: LDG, LDG, DFMA, LDG, DFMA ...);
+    // the thread's eight 16-byte pieces are requested up front as L1 prefetches
+#pragma unroll
+    for (int t = 0; t < kMDC; ++t)
+      if (k0 + t < k) asm volatile("prefetch.global.L1 [%0];" ::"l"(V + (k0 + t) * ld2 + i));
     const double2 wi = w[i];
 #pragma unroll
     for (int t = 0; t < kMDC; ++t)
